@@ -1,0 +1,26 @@
+// Device side of the execute step: kernel instantiation from a complete schedule and launch.
+// Implemented in csrc/kernels/*.cu (nvcc, sm_100a). The host library reaches the GPU only
+// through these functions.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "hw.hpp"
+#include "op.hpp"
+#include "sched.hpp"
+
+namespace gb::dev {
+
+struct Kernel;  // opaque: the instantiated plan + device workspace
+
+Kernel* prepare(const OpDesc& op, const Sched& s, int variant);  // throws gb::Error
+void destroy(Kernel* k);
+std::string info(const Kernel* k);
+void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream);
+void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, void* stream);
+
+DeviceLimits query(int device);  // cudaGetDeviceProperties -> limits (peaks filled by caller)
+uint64_t launch_count();
+
+}  // namespace gb::dev
