@@ -1,5 +1,6 @@
 // Execute step: instantiate a kernel family from a complete schedule and launch it.
 // This is the device replacement of the SPEC's lower()+interpret().
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <sstream>
@@ -16,7 +17,9 @@ namespace gb::dev {
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
-}
+
+const char* kVariantNames[] = {"simt_parity", "simt_f32", "tc_tf32", "tc_bf16", "stream"};
+}  // namespace
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(Code::Cuda, std::string(what) + ": " + cudaGetErrorString(e));
@@ -25,7 +28,7 @@ void check_cuda(cudaError_t e, const char* what) {
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-enum class Family { Generic };
+enum class Family { Generic, GemmTc, ConvTc };
 
 struct Kernel {
   OpDesc op;
@@ -34,23 +37,57 @@ struct Kernel {
   Family family = Family::Generic;
   GenericPlan gplan{};
   bool f64 = false;
+  GemmTcArgs gemm;
+  ConvTcArgs conv;
+  int launches = 1;
+  std::string plan_info;
+  void* ws = nullptr;  // family workspace
   // host-buffer execute staging (allocated on first use)
   void* d_in[3] = {nullptr, nullptr, nullptr};
   void* d_out = nullptr;
-  size_t in_bytes[3] = {0, 0, 0};
-  size_t out_bytes = 0;
-  int launches = 1;
 };
 
 namespace {
 
-int resolve_variant(const OpDesc& op, int variant) {
-  if (variant != -1) return variant;
-  return 1;  // SIMT_F32 until the tensor-core / stream families take over
-}
-
 size_t tensor_bytes(const OpDesc& op, int t) {
   return static_cast<size_t>(op.tensor_elems(t, false)) * op.dtype_bytes * static_cast<size_t>(op.batch);
+}
+
+int64_t pow2_clamp(int64_t v, int64_t lo, int64_t hi) {
+  int64_t p = lo;
+  while (p < v && p < hi) p <<= 1;
+  return p;
+}
+
+bool gemm_tc_ok(const OpDesc& op, bool bf16) {
+  if (op.kind != Kind::Gemm) return false;
+  if (bf16 != (op.dtype_bytes == 2)) return false;  // operands are read in their stored dtype
+  return gemm_tc_supported(static_cast<int>(op.param("M")), static_cast<int>(op.param("N")),
+                           static_cast<int>(op.param("K")), op.dtype_bytes);
+}
+
+bool conv_tc_ok(const OpDesc& op, bool bf16) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4) return false;
+  return conv_tc_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
+                           static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
+                           static_cast<int>(op.stride), bf16);
+}
+
+int resolve_variant(const OpDesc& op, int variant) {
+  if (variant != -1) return variant;
+  if (op.kind == Kind::Gemm && op.dtype_bytes == 2 && gemm_tc_ok(op, true)) return 3;
+  if (op.kind == Kind::Gemm && gemm_tc_ok(op, false)) return 2;
+  if (op.kind == Kind::Conv2d && conv_tc_ok(op, false)) return 2;
+  return 1;
+}
+
+int current_device_sms(int* optin_smem) {
+  int dev = 0, sms = 0, optin = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem optin");
+  if (optin_smem) *optin_smem = optin;
+  return sms;
 }
 
 }  // namespace
@@ -80,25 +117,72 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
   k->op = op;
   k->state = s;
   k->variant = resolve_variant(op, variant);
+  std::ostringstream pi;
   try {
+    int optin = 0;
+    const int sms = current_device_sms(&optin);
     switch (k->variant) {
       case 0:
       case 1: {
-        int dev = 0, optin = 0;
-        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-        check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem optin");
         k->f64 = k->variant == 0;
         k->family = Family::Generic;
         k->gplan = lower_generic(op, s, generic_max_width(k->f64), op.dtype_bytes, optin);
+        pi << plan_json(k->gplan);
+        break;
+      }
+      case 2:
+      case 3: {
+        const bool bf16 = k->variant == 3;
+        if (op.kind == Kind::Gemm && gemm_tc_ok(op, bf16)) {
+          k->family = Family::GemmTc;
+          GemmTcArgs& g = k->gemm;
+          g.M = static_cast<int>(op.param("M"));
+          g.N = static_cast<int>(op.param("N"));
+          g.K = static_cast<int>(op.param("K"));
+          g.batch = static_cast<int>(op.batch);
+          g.bf16 = bf16;
+          // N tile from the schedule's level-1 n tile (UMMA N in [64, 256]); M tile = UMMA M 128
+          g.BN = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, 256));
+          pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"grid\":["
+             << (g.N + g.BN - 1) / g.BN << "," << (g.M + 127) / 128 << "," << g.batch << "],\"block\":192}";
+        } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
+          k->family = Family::ConvTc;
+          k->launches = 3;
+          ConvTcArgs& c = k->conv;
+          c.N = static_cast<int>(op.param("N"));
+          c.C = static_cast<int>(op.param("C"));
+          c.H = static_cast<int>(op.param("H"));
+          c.W = static_cast<int>(op.param("W"));
+          c.F = static_cast<int>(op.param("F"));
+          c.R = static_cast<int>(op.param("R"));
+          c.S = static_cast<int>(op.param("S"));
+          c.OH = static_cast<int>(op.param("OH"));
+          c.OW = static_cast<int>(op.param("OW"));
+          c.bf16 = bf16;
+          c.sms = sms;
+          const size_t es = bf16 ? 2 : 4;
+          const size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
+          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
+          check_cuda(cudaMalloc(&k->ws, xb + wb + 256), "conv workspace");
+          c.ws_x = k->ws;
+          c.ws_w = static_cast<char*>(k->ws) + ((xb + 255) & ~size_t(255));
+          const int tiles = c.N * ((c.OH + 3) / 4) * ((c.OW + 31) / 32);
+          pi << "{\"family\":\"conv_tc\",\"M_tile\":\"4x32 positions\",\"FN\":" << c.F << ",\"tiles\":" << tiles
+             << ",\"grid\":" << std::min(tiles, sms) << ",\"block\":192,\"prepass\":\"nchw->nhwc, kfcrs->rsfc\"}";
+        } else {
+          throw Error(Code::Unsupported, std::string(kVariantNames[k->variant]) + " not available for " + op.label());
+        }
         break;
       }
       default:
         throw Error(Code::Unsupported, "variant " + std::to_string(variant) + " not available for " + op.label());
     }
   } catch (...) {
+    if (k->ws) cudaFree(k->ws);
     delete k;
     throw;
   }
+  k->plan_info = pi.str();
   return k;
 }
 
@@ -107,21 +191,21 @@ void destroy(Kernel* k) {
   for (void* p : k->d_in)
     if (p) cudaFree(p);
   if (k->d_out) cudaFree(k->d_out);
+  if (k->ws) cudaFree(k->ws);
   delete k;
 }
 
 std::string info(const Kernel* k) {
   std::ostringstream os;
-  static const char* names[] = {"simt_parity", "simt_f32", "tc_tf32", "tc_bf16", "stream"};
-  os << "{\"variant\":" << k->variant << ",\"variant_name\":\"" << names[k->variant] << "\",\"op\":" << k->op.to_json()
-     << ",\"state\":" << k->state.to_json(k->op) << ",\"flops\":" << json::num(k->op.flops_true())
-     << ",\"bytes\":" << json::num(k->op.bytes_true()) << ",\"launches\":" << k->launches << ",\"plan\":";
-  os << plan_json(k->gplan);
-  os << "}";
+  os << "{\"variant\":" << k->variant << ",\"variant_name\":\"" << kVariantNames[k->variant]
+     << "\",\"op\":" << k->op.to_json() << ",\"state\":" << k->state.to_json(k->op)
+     << ",\"flops\":" << json::num(k->op.flops_true()) << ",\"bytes\":" << json::num(k->op.bytes_true())
+     << ",\"launches\":" << k->launches << ",\"plan\":" << k->plan_info << "}";
   return os.str();
 }
 
-void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream) {
+void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, void* stream) {
+  auto* k = const_cast<Kernel*>(kc);  // tensor-map caches only; results do not depend on them
   const OpDesc& op = k->op;
   if (n_in != op.input_count())
     throw Error(Code::ShapeMismatch,
@@ -134,6 +218,12 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
       launch_generic(k->gplan, k->f64, op.dtype_bytes == 2, d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out,
                      static_cast<int>(op.batch), st);
       break;
+    case Family::GemmTc:
+      launch_gemm_tc(k->gemm, d_in[0], d_in[1], d_out, st);
+      break;
+    case Family::ConvTc:
+      launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st);
+      break;
   }
 }
 
@@ -145,17 +235,11 @@ void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, voi
   auto st = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_in; ++i) {
     const size_t b = tensor_bytes(op, i);
-    if (!k->d_in[i]) {
-      check_cuda(cudaMalloc(&k->d_in[i], b), "cudaMalloc input staging");
-      k->in_bytes[i] = b;
-    }
+    if (!k->d_in[i]) check_cuda(cudaMalloc(&k->d_in[i], b), "cudaMalloc input staging");
     check_cuda(cudaMemcpyAsync(k->d_in[i], h_in[i], b, cudaMemcpyHostToDevice, st), "H2D");
   }
   const size_t ob = tensor_bytes(op, op.output_index());
-  if (!k->d_out) {
-    check_cuda(cudaMalloc(&k->d_out, ob), "cudaMalloc output staging");
-    k->out_bytes = ob;
-  }
+  if (!k->d_out) check_cuda(cudaMalloc(&k->d_out, ob), "cudaMalloc output staging");
   execute(k, k->d_in, n_in, k->d_out, stream);
   check_cuda(cudaMemcpyAsync(h_out, k->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
   check_cuda(cudaStreamSynchronize(st), "stream sync");

@@ -1,14 +1,49 @@
 // Host-callable launchers of the kernel families (all asynchronous on the given stream).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 
 #include "plan.h"
 
 namespace gb::dev {
 
+// ---- state-driven SIMT family (generic.cu) ----
 int generic_max_width(bool f64);
 void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, const void* in1, void* out,
                     int batch, cudaStream_t st);
+
+// ---- TMA tensor maps (gemm_tc.cu) ----
+void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
+                const uint64_t* strides_bytes, const uint32_t* box, bool atom32 = false);
+
+// ---- tensor-core GEMM family (gemm_tc.cu) ----
+struct GemmTcArgs {
+  CUtensorMap mapA, mapB;  // rebuilt when the operand pointers change
+  const void* last_A = nullptr;
+  const void* last_B = nullptr;
+  void* C = nullptr;
+  int M = 0, N = 0, K = 0, batch = 1, BN = 128;
+  bool bf16 = false;
+};
+bool gemm_tc_supported(int M, int N, int K, int elem_bytes);
+void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaStream_t st);
+
+// ---- tensor-core implicit-GEMM conv2d family (conv_tc.cu) ----
+struct ConvTcArgs {
+  CUtensorMap mapX, mapW;  // over the workspace layouts, built once
+  bool maps_ready = false;
+  const void* last_I = nullptr;
+  const void* last_K = nullptr;
+  void* ws_x = nullptr;  // NHWC input copy
+  void* ws_w = nullptr;  // [R][S][F][C] filter copy
+  int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
+  int sms = 148;
+  bool bf16 = false;
+};
+bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
+size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
+void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st);
 
 }  // namespace gb::dev

@@ -1,0 +1,132 @@
+"""GPU parity of the tensor-core families (tcgen05) against the CPU oracle.
+
+Bars (stated per variant):
+  * integer-valued inputs U{-2..2}: BIT-EXACT for tc_tf32 and tc_bf16 (every product and partial
+    sum is exactly representable; fp32 accumulation of integers < 2^24 is exact);
+  * U(-1,1) inputs: tc_tf32  max|gpu - oracle| / max|oracle| <= TF32_TOL
+                    tc_bf16  (bf16 operands)  <= BF16_TOL.
+Includes the BASELINE configurations at full size (G, C, B).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import CONFIG_OPS
+
+TF32_TOL = 2e-3
+BF16_TOL = 1e-2
+
+torch = pytest.importorskip("torch")
+g = pytest.importorskip("paper_2502_11407_b200")
+from oracle import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+_HW = {}
+
+
+def hw():
+    if "b200" not in _HW:
+        _HW["b200"] = g.HardwareSpec.b200(0)
+    return _HW["b200"]
+
+
+def inputs(op, rng, integer):
+    xs = []
+    for t in op.tensors[:-1]:
+        n = int(np.prod(t["true_dims"])) * op.batch
+        x = rng.integers(-2, 3, size=n).astype(np.float32) if integer else rng.uniform(-1, 1, n).astype(np.float32)
+        if op.dtype_bytes == 2:
+            x = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+        xs.append(x)
+    return xs
+
+
+def run(op, sched, variant, xs, nout):
+    bf16 = op.dtype_bytes == 2
+    k = g.Kernel(op, sched, 0, variant)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    dev = [torch.from_numpy(x).to(dt).cuda() for x in xs]
+    out = torch.full((nout,), float("nan"), dtype=dt, device="cuda")
+    k.execute(dev, out)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy().astype(np.float64), k.info
+
+
+def check(doc, variant, tol, seed=0, top_k=1):
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, hw(), g.EngineConfig(seed=seed, mode="b200", top_k=top_k))
+    rng = np.random.default_rng(seed)
+    bf16_out = op.dtype_bytes == 2
+    xi = inputs(op, rng, integer=True)
+    ref = O.reference_compute(doc, xi, threads=8)
+    got, info = run(op, sched, variant, xi, ref.size)
+    exp = ref.astype(np.float32).astype(np.float64)
+    assert np.array_equal(got, exp), (info["plan"], np.nanmax(np.abs(got - exp)))
+    xr = inputs(op, rng, integer=False)
+    ref = O.reference_compute(doc, xr, threads=8)
+    got, info = run(op, sched, variant, xr, ref.size)
+    err = np.nanmax(np.abs(got - ref)) / np.abs(ref).max()
+    assert not np.isnan(got).any()
+    assert err <= tol, (info["plan"], err)
+    return info
+
+
+GEMMS = [
+    {"kind": "gemm", "M": 128, "K": 64, "N": 64},
+    {"kind": "gemm", "M": 256, "K": 256, "N": 256},
+    {"kind": "gemm", "M": 200, "K": 96, "N": 136},  # ragged M/N tiles, N % 16 != 0
+    {"kind": "gemm", "M": 64, "K": 1000, "N": 72},  # K tail inside the last 128 B chunk
+]
+
+
+@pytest.mark.parametrize("doc", GEMMS, ids=lambda d: f"{d['M']}x{d['K']}x{d['N']}")
+def test_gemm_tf32(doc):
+    info = check(doc, "tc_tf32", TF32_TOL)
+    assert info["plan"]["family"] == "gemm_tc"
+
+
+BGEMMS = [
+    {"kind": "gemm", "M": 128, "K": 64, "N": 128, "dtype_bytes": 2, "batch": 3},
+    {"kind": "gemm", "M": 96, "K": 48, "N": 80, "dtype_bytes": 2, "batch": 2},
+    {"kind": "gemm", "M": 256, "K": 192, "N": 256, "dtype_bytes": 2},
+]
+
+
+@pytest.mark.parametrize("doc", BGEMMS, ids=lambda d: f"{d['M']}x{d['K']}x{d['N']}b{d.get('batch', 1)}")
+def test_gemm_bf16(doc):
+    info = check(doc, "tc_bf16", BF16_TOL)
+    assert info["plan"]["family"] == "gemm_tc"
+
+
+CONVS = [
+    {"kind": "conv2d", "I": [2, 8, 12, 12], "K": [16, 8, 3, 3], "S": 1},
+    {"kind": "conv2d", "I": [1, 32, 20, 40], "K": [64, 32, 3, 3], "S": 1},
+    {"kind": "conv2d", "I": [2, 64, 10, 70], "K": [40, 64, 1, 1], "S": 1},  # 1x1, F not a power of two
+    {"kind": "conv2d", "I": [1, 16, 9, 35], "K": [64, 16, 5, 3], "S": 1},
+]
+
+
+@pytest.mark.parametrize("doc", CONVS, ids=lambda d: json.dumps(d["I"] + d["K"]))
+@pytest.mark.parametrize("variant,tol", [("tc_tf32", TF32_TOL), ("tc_bf16", BF16_TOL)])
+def test_conv_tc(doc, variant, tol):
+    info = check(doc, variant, tol)
+    assert info["plan"]["family"] == "conv_tc"
+
+
+@pytest.mark.parametrize("name,variant,tol", [("G", "tc_tf32", TF32_TOL), ("C", "tc_tf32", TF32_TOL),
+                                              ("C", "tc_bf16", BF16_TOL), ("B", "tc_bf16", BF16_TOL)])
+def test_baseline_configs_full_size(name, variant, tol):
+    doc = dict(CONFIG_OPS[name])
+    if name == "B":
+        doc["batch"] = 192
+    check(doc, variant, tol)
+
+
+def test_auto_picks_tensor_cores():
+    for name in ("G", "C"):
+        op = g.TensorOpSpec.parse_text(json.dumps(CONFIG_OPS[name]))
+        sched = g.optimize(op, hw(), g.EngineConfig(mode="b200", top_k=1))
+        k = g.Kernel(op, sched, 0, "auto")
+        assert k.info["variant_name"] == "tc_tf32"
