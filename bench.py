@@ -1,0 +1,495 @@
+#!/usr/bin/env python
+"""Constructed-kernel throughput on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload conv2d]
+
+A step = one execute of the hot path (operator description -> constructed schedule ->
+instantiated sm_100a kernel) over one batch of synthetic input of the BASELINE shape.
+  value      device time of the execute (CUDA events on the launching stream), inputs resident
+             in HBM, L2 flushed (256 MiB write) between steps; whole-job throughput over ranks
+  e2e        the same through the C-ABI host-buffer call gensor_execute_host (pinned host
+             inputs -> H2D -> execute -> D2H -> sync), CUDA events around each call
+  roofline   the dominant kernel's own launches (events around each internal launch)
+  cpu_baseline  the oracle's interpret() of the same schedule on a bounded sample, all host threads
+  --impl reference  the reference's CPU path: its own construct library (oracle/_ref, unmodified
+             proj/src) + the restated interpreter (its executor lowering.cpp is absent)
+Multi-GPU (torchrun): each rank executes its own replica (batch-sharded layer; no collective on
+the compute path — "scaling": "weak"); the process group is used only for the barrier and the
+max-over-ranks reduction of the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "constructed-kernel TFLOP/s or GB/s and % roofline per op; construction time (s)"
+
+# BASELINE.json configs as reference op specs. conv2d is configs[1], the metric's
+# single-GPU headline; the others run as the per-op suite.
+WORKLOADS = {
+    "conv2d": dict(op={"kind": "conv2d", "I": [16, 64, 58, 58], "K": [64, 64, 3, 3], "S": 1},
+                   name="Conv2d ResNet-50 layer N=16 56x56x64->64 3x3 stride 1 (implicit GEMM, pre-padded 58x58 input)",
+                   bound="tensor", unit="TFLOP/s"),
+    "gemm": dict(op={"kind": "gemm", "M": 1024, "K": 1024, "N": 1024},
+                 name="GEMM fp32 M=N=K=1024", bound="tensor", unit="TFLOP/s"),
+    "bgemm": dict(op={"kind": "gemm", "M": 512, "K": 64, "N": 512, "dtype_bytes": 2, "batch": 192},
+                  name="Batched GEMM bf16 B*H=192 512x64x512 (attention QK^T shape)", bound="hbm", unit="TFLOP/s"),
+    "rowsum": dict(op={"kind": "gemv", "M": 32768, "N": 4096},
+                   name="Row reduction 32768x4096 fp32 (gemv, x=1)", bound="hbm", unit="GB/s", ones_x=True),
+    "softmax": dict(op={"kind": "softmax", "M": 32768, "N": 4096},
+                    name="Softmax 32768x4096 fp32 (row-wise)", bound="hbm", unit="GB/s"),
+    "dwconv": dict(op={"kind": "dwconv2d", "I": [32, 256, 114, 114], "K": [256, 1, 3, 3], "S": 1},
+                   name="Depthwise conv 3x3 fp32 32x256x112x112", bound="hbm", unit="GB/s"),
+    "avgpool": dict(op={"kind": "avgpool2d", "I": [32, 256, 114, 114], "F": 3, "S": 1},
+                    name="AvgPool 3x3 s1 fp32 32x256x112x112", bound="hbm", unit="GB/s"),
+}
+SUITE_DEFAULT = ["gemm", "bgemm", "rowsum", "softmax", "dwconv", "avgpool"]
+
+# the B200 in the reference's own hardware format (for oracle/_ref).
+B200_REF_HW = {
+    "name": "b200-nominal", "peak_flops": 7.2e13, "clock_hz": 1.9e9,
+    "levels": [
+        {"name": "hbm3e", "capacity_bytes": "unlimited", "bandwidth_bytes_per_cycle": 4210, "latency_cycles": 800,
+         "bank_width_elems": 0},
+        {"name": "smem", "capacity_bytes": 232448, "bandwidth_bytes_per_cycle": 18944, "latency_cycles": 30,
+         "bank_width_elems": 32},
+        {"name": "regs", "capacity_bytes": 1020, "bandwidth_bytes_per_cycle": 227328, "latency_cycles": 1,
+         "bank_width_elems": 0},
+    ],
+}
+
+
+def measured_peaks() -> dict:
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            d["source"] = "measured (MEASURED_PEAKS.json)"
+            return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc = device, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200", "-i",
+                 str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+def make_inputs(op, spec, rng, torch, device):
+    """Synthetic inputs U(-1,1) of the op's true shapes (bf16 for dtype_bytes 2); rowsum x = 1."""
+    dt = torch.bfloat16 if op.dtype_bytes == 2 else torch.float32
+    xs = []
+    for i, t in enumerate(op.tensors[:-1]):
+        n = int(np.prod(t["true_dims"])) * op.batch
+        if spec.get("ones_x") and i == 1:
+            x = torch.ones(n, dtype=dt, device=device)
+        else:
+            x = (torch.rand(n, device=device, generator=rng) * 2 - 1).to(dt)
+        xs.append(x)
+    nout = int(np.prod(op.tensors[-1]["true_dims"])) * op.batch
+    out = torch.empty(nout, dtype=dt, device=device)
+    return xs, out
+
+
+def tf32_peak(torch, device) -> float:
+    """cuBLAS TF32 GEMM 8192^3, best of 5 (denominator for the tf32 tensor-core kernels)."""
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device=device)
+    b = torch.randn(8192, 8192, device=device)
+    for _ in range(2):
+        a @ b
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    del a, b
+    return 2 * 8192 ** 3 / best / 1e12
+
+
+def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None, e2e=True, timing=True):
+    """Construct + instantiate + time one op. Returns a dict of measurements (this rank)."""
+    op = g.TensorOpSpec.parse_text(json.dumps(spec["op"]))
+    cfg = g.EngineConfig(seed=0, mode="b200")
+    con = []
+    sched = None
+    for _ in range(5):
+        t0 = time.perf_counter()
+        sched = g.optimize(op, hw, cfg)
+        con.append(time.perf_counter() - t0)
+    k = g.Kernel(op, sched, 0, variant)
+    rng = torch.Generator(device=device)
+    rng.manual_seed(0)
+    xs, out = make_inputs(op, spec, rng, torch, device)
+    stream = torch.cuda.current_stream(device)
+    if timing:
+        k.set_timing(True)
+    for _ in range(warmup):
+        k.execute(xs, out, stream)
+    torch.cuda.synchronize(device)
+
+    step_ms, launch_ms = [], {}
+    n0 = g.launch_count()
+    for _ in range(steps):
+        if flush is not None:
+            flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        k.execute(xs, out, stream)
+        e.record(stream)
+        e.synchronize()
+        step_ms.append(s.elapsed_time(e))
+        if timing:
+            for name, ms in k.timings():
+                launch_ms.setdefault(name, []).append(ms)
+    launches = g.launch_count() - n0
+    res = dict(op=op, kernel=k, sched=sched, step_ms=step_ms, launch_ms=launch_ms, launches=launches,
+               construct_s=statistics.median(con), flops=op.flops, bytes=op.bytes)
+    if e2e:
+        hin = [x.cpu().pin_memory() for x in xs]
+        hout = torch.empty(out.numel(), dtype=out.dtype).pin_memory()
+        k.set_timing(False)
+        k.execute_host(hin, hout, stream)  # warm the staging buffers
+        e2e_ms = []
+        for _ in range(max(3, steps // 2)):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            k.execute_host(hin, hout, stream)
+            e.record(stream)
+            e.synchronize()
+            e2e_ms.append(s.elapsed_time(e))
+        res["e2e_ms"] = e2e_ms
+        res["h2d"] = sum(x.numel() * x.element_size() for x in hin)
+        res["d2h"] = hout.numel() * hout.element_size()
+        if not torch.equal(hout.to(device), out):
+            raise RuntimeError("host-buffer execute disagrees with device execute")
+    return res
+
+
+def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=None):
+    name, ms = max(res["launch_ms"].items(), key=lambda kv: statistics.mean(kv[1]))
+    avg = statistics.mean(ms) / 1e3
+    if spec["bound"] == "tensor":
+        achieved = res["flops"] / avg / 1e12
+        if variant_name == "tc_tf32":
+            peak, src = tf32_tflops, "cuBLAS tf32 8192^3 measured in this run (best of 5)"
+        else:
+            peak, src = peaks["bf16_tflops"], f"bf16 dense, {peaks['source']}"
+        r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+             "traffic": traffic, "kernel": name, "peak_source": src,
+             "share_of_step": statistics.mean(ms) / statistics.mean(res["step_ms"])}
+    else:
+        achieved = res["bytes"] / avg / 1e9
+        peak = peaks["hbm_gbs"]
+        r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+             "traffic": traffic, "kernel": name, "peak_source": f"hbm copy, {peaks['source']}",
+             "share_of_step": statistics.mean(ms) / statistics.mean(res["step_ms"])}
+    r["algorithmic_per_launch"] = res["flops"] if spec["bound"] == "tensor" else res["bytes"]
+    return r
+
+
+def ncu_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(workload)
+    return None
+
+
+def cpu_baseline(spec, sched_state, budget_s=12.0):
+    """The oracle's interpret() of the constructed schedule on a bounded sample, all threads."""
+    from oracle import oracle as O
+
+    doc = dict(spec["op"])
+    threads = os.cpu_count() or 1
+    kind = doc["kind"]
+    # sample: shrink the outermost batch-like dimension
+    if kind in ("conv2d", "dwconv2d", "avgpool2d"):
+        full = doc["I"][0]
+        key = ("I", 0)
+    elif kind == "gemm":
+        full = doc.get("batch", 1) if doc.get("batch", 1) > 1 else doc["M"]
+        key = ("batch",) if doc.get("batch", 1) > 1 else ("M",)
+    else:
+        full = doc["M"]
+        key = ("M",)
+
+    def sized(n):
+        d = json.loads(json.dumps(doc))
+        if key[0] == "I":
+            d["I"][0] = n
+        else:
+            d[key[0]] = n
+        return d
+
+    def run(n):
+        d = sized(n)
+        import paper_2502_11407_b200 as g
+
+        op = g.TensorOpSpec.parse_text(json.dumps(d))
+        # the sample shrinks one extent: clamp the schedule's tiles to the sample's padded extents
+        st = {"tiles": [[min(t, a["padded"]) for t in per] for per, a in zip(sched_state["tiles"], op.axes)],
+              "vthreads": [min(v, min(a["padded"], per[-1]) if per else v)
+                           for v, per, a in zip(sched_state["vthreads"], sched_state["tiles"], op.axes)]}
+        rng = np.random.default_rng(0)
+        xs = [rng.uniform(-1, 1, int(np.prod(t["true_dims"])) * op.batch).astype(np.float32)
+              for t in op.tensors[:-1]]
+        t0 = time.perf_counter()
+        O.interpret(d, st, xs, threads=threads)
+        return time.perf_counter() - t0, op.flops, op.bytes
+
+    n = 1
+    dt, fl, by = run(n)
+    while dt < budget_s / 4 and n < full:
+        n = min(full, n * 2 if dt < budget_s / 8 else n + 1)
+        dt, fl, by = run(n)
+    unit = spec["unit"]
+    value = fl / dt / 1e12 if unit == "TFLOP/s" else by / dt / 1e9
+    return {"value": value, "unit": unit, "cores": threads, "kind": "port",
+            "sample": f"{kind} with the outer dim {key[0]}={n} of {full}: {fl:.3e} FLOP in {dt:.2f} s "
+                      f"(oracle/gensor_oracle.c interpret() of the same schedule, OpenMP {threads} threads)"}
+
+
+def reference_construct_s(spec):
+    from oracle import ref
+
+    if not ref.available():
+        return None
+    r = ref.optimize(spec["op"], B200_REF_HW, {"seed": 0})
+    return r.get("wall_s")
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference's CPU path (construct with its own library + the
+    restated interpreter), rank 0 only, all host threads, bounded sample per step."""
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return
+    spec = WORKLOADS[args.workload]
+    from oracle import oracle as O, ref
+
+    import paper_2502_11407_b200 as g
+
+    op_doc = spec["op"]
+    if ref.available():
+        con = ref.optimize(op_doc, B200_REF_HW, {"seed": 0})
+        state = con["results"][0]["state"]
+        construct_kind = "reference (oracle/_ref: unmodified proj/src)"
+    else:  # reference sources absent on this box: same schedule from the bit-identical port
+        op = g.TensorOpSpec.parse_text(json.dumps(op_doc))
+        hw = g.HardwareSpec.load_text(json.dumps(B200_REF_HW))
+        state = g.optimize(op, hw, g.EngineConfig(seed=0))[0]["state"]
+        construct_kind = "port (reference-compatible engine, bit-identical)"
+    base = cpu_baseline(spec, state, budget_s=args.ref_budget)
+    times = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if ref.available():
+            ref.optimize(op_doc, B200_REF_HW, {"seed": 0})
+        times.append(time.perf_counter() - t0)
+    con_s = statistics.median(times[args.warmup:]) if times[args.warmup:] else None
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": spec["unit"],
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 accumulate (fp32 data)", "data": "synthetic U(-1,1)",
+            "config": {"workload": spec["name"], "op": op_doc, "parallelism": "rank 0 only, host cores"},
+            "cpu_baseline": {**base},
+            "e2e": {"value": base["value"], "unit": spec["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "construction_s": con_s, "construction_kind": construct_kind, "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2502_11407_b200 as g
+
+    ws, rank, local = dist_info()
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+        pg = dist
+    peaks = measured_peaks()
+    hw = g.HardwareSpec.b200(local, {"hbm_gbs": peaks["hbm_gbs"], "bf16_tflops": peaks["bf16_tflops"]})
+    tf32 = tf32_peak(torch, device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # 2x L2: flushed between steps
+
+    spec = WORKLOADS[args.workload]
+
+    def barrier():
+        torch.cuda.synchronize(device)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize(device)
+
+    barrier()
+    with ClockSampler(local) as clk:
+        res = run_op(g, torch, spec, hw, args.steps, args.warmup, device, args.variant, flush)
+    barrier()
+    total_ms = sum(res["step_ms"])
+    e2e_ms = statistics.mean(res["e2e_ms"])
+    if pg:
+        t = torch.tensor([total_ms, e2e_ms], device=device, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms, e2e_ms = t.tolist()
+    ms_step = total_ms / args.steps
+    work = res["flops"] if spec["unit"] == "TFLOP/s" else res["bytes"]
+    scale = 1e12 if spec["unit"] == "TFLOP/s" else 1e9
+    value = ws * work / (ms_step / 1e3) / scale
+    e2e_value = ws * work / (e2e_ms / 1e3) / scale
+    info = res["kernel"].info
+    rl = roofline(res, spec, peaks, tf32, info["variant_name"], ncu_traffic(args.workload))
+
+    suite = {}
+    if args.suite and ws == 1:
+        for wname in args.suite.split(","):
+            if not wname or wname == args.workload:
+                continue
+            try:
+                r = run_op(g, torch, WORKLOADS[wname], hw, max(5, args.steps), max(3, args.warmup), device, "auto",
+                           flush, e2e=False)
+                ki = r["kernel"].info
+                sp = WORKLOADS[wname]
+                w = r["flops"] if sp["unit"] == "TFLOP/s" else r["bytes"]
+                suite[wname] = {
+                    "op": sp["op"], "variant": ki["variant_name"], "family": ki["plan"].get("family"),
+                    "schedule": ki["state"]["repr"],
+                    "value": w / (statistics.mean(r["step_ms"]) / 1e3) / (1e12 if sp["unit"] == "TFLOP/s" else 1e9),
+                    "unit": sp["unit"], "ms_per_step": statistics.mean(r["step_ms"]),
+                    "roofline": roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname)),
+                    "construction_s": r["construct_s"],
+                }
+                del r
+            except Exception as exc:  # keep the headline line even if a suite op fails
+                suite[wname] = {"error": str(exc)[:300]}
+            torch.cuda.empty_cache()
+
+    base = None
+    ref_con = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(spec, res["sched"][0]["state"], budget_s=args.ref_budget)
+        ref_con = reference_construct_s(spec)
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": spec["unit"], "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {"tc_tf32": "tf32 (fp32 storage, fp32 accumulate)", "tc_bf16": "bf16 (fp32 accumulate)",
+                  "simt_f32": "f32", "simt_parity": "f64 accumulate", "stream": "f32"}[info["variant_name"]],
+        "data": "synthetic U(-1,1)",
+        "config": {"workload": spec["name"], "op": spec["op"], "variant": info["variant_name"],
+                   "schedule": info["state"]["repr"], "kernel_plan": info["plan"], "engine": "b200 mode",
+                   "l2": "flushed between steps (256 MiB write outside the events)",
+                   "parallelism": f"weak: {ws} independent replica(s), one per GPU (batch-sharded layer), no collective"},
+        "roofline": rl,
+        "e2e": {"value": e2e_value, "unit": spec["unit"], "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
+                "path": "gensor_execute_host (pinned host buffers)"},
+        "gpu_launches": res["launches"],
+        "construction_s": res["construct_s"],
+        "construction_reference_s": ref_con,
+        "clocks": clk.summary(),
+        "cpu_baseline": base,
+        "suite": suite or None,
+    }
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="conv2d")
+    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

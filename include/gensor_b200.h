@@ -160,6 +160,12 @@ int gensor_execute_host(gensor_kernel* k, const void* const* h_inputs, int n_inp
                         void* stream);
 void gensor_kernel_free(gensor_kernel* k);
 
+/* Per-launch device timing (CUDA events recorded on the execute stream around every internal
+ * launch). While enabled, gensor_kernel_timings() returns the durations of the LAST execute's
+ * launches in ms (synchronising on its events) and their names as a JSON array in `names`. */
+int gensor_kernel_set_timing(gensor_kernel* k, int enable);
+int gensor_kernel_timings(gensor_kernel* k, float* ms, int cap, int* n, char* names, size_t names_cap);
+
 /* Number of kernels this library launched since load (process-wide counter). */
 uint64_t gensor_launch_count(void);
 

@@ -438,4 +438,29 @@ void gensor_kernel_free(gensor_kernel* k) {
 
 uint64_t gensor_launch_count(void) { return gb::dev::launch_count(); }
 
+int gensor_kernel_set_timing(gensor_kernel* k, int enable) {
+  if (!k) return fail(GENSOR_EINVALID, "null kernel");
+  return guarded([&]() -> int {
+    gb::dev::set_timing(k->k, enable != 0);
+    return GENSOR_OK;
+  });
+}
+
+int gensor_kernel_timings(gensor_kernel* k, float* ms, int cap, int* n, char* names, size_t names_cap) {
+  if (!k || !n) return fail(GENSOR_EINVALID, "null argument");
+  return guarded([&]() -> int {
+    auto t = gb::dev::timings(k->k);
+    *n = static_cast<int>(t.size());
+    std::string js = "[";
+    for (size_t i = 0; i < t.size(); ++i) {
+      if (ms && static_cast<int>(i) < cap) ms[i] = t[i].second;
+      js += (i ? "," : "") + gb::json::quote(t[i].first);
+    }
+    js += "]";
+    size_t need = 0;
+    if (names) return emit(js, names, names_cap, &need);
+    return GENSOR_OK;
+  });
+}
+
 }  // extern "C"

@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "hw.hpp"
 #include "op.hpp"
@@ -19,6 +21,9 @@ void destroy(Kernel* k);
 std::string info(const Kernel* k);
 void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream);
 void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, void* stream);
+
+void set_timing(Kernel* k, bool on);
+std::vector<std::pair<std::string, float>> timings(Kernel* k);  // last execute, per launch (ms)
 
 DeviceLimits query(int device);  // cudaGetDeviceProperties -> limits (peaks filled by caller)
 uint64_t launch_count();

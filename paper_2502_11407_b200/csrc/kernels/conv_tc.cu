@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <typename T, int FN>
-void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st) {
+void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
   constexpr int CK = 128 / sizeof(T);
   const int nck = (a.C + CK - 1) / CK;
   const size_t w_bytes = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
@@ -235,14 +235,17 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
   T* X = static_cast<T*>(a.ws_x);
   T* Wt = static_cast<T*>(a.ws_w);
   // pre-pass: layouts for TMA
+  mk.mark(st);
   {
     dim3 grid((a.W + 31) / 32, (a.C + 31) / 32, a.N * a.H);
     k_nchw_to_nhwc<T><<<grid, 256, 0, st>>>(I, X, a.C, a.H, a.W);
     check_cuda(cudaGetLastError(), "nchw_to_nhwc");
+    mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     k_weights_rsfc<T><<<static_cast<unsigned>(std::min<int64_t>(1184, (wt + 255) / 256)), 256, 0, st>>>(
         K, Wt, a.F, a.C, a.R, a.S);
     check_cuda(cudaGetLastError(), "weights_rsfc");
+    mk.mark(st);
     count_launch(2);
   }
   if (!a.maps_ready) {
@@ -273,6 +276,7 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     const int grid = std::min(total, a.sms);
     kern<<<grid, 192, smem, st>>>(a.mapX, a.mapW, O, a.F, a.C, a.R, a.S, a.OH, a.OW, tiles_h, tiles_w, total);
     check_cuda(cudaGetLastError(), "conv_tc launch");
+    mk.mark(st);
     count_launch();
   };
   if (stages >= 4)
@@ -301,7 +305,7 @@ bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
          conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256;
 }
 
-void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st) {
+void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {
   if (I != a.last_I || K != a.last_K) a.last_I = I, a.last_K = K;
   const float* i = static_cast<const float*>(I);
   const float* k = static_cast<const float*>(K);
@@ -310,17 +314,17 @@ void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaSt
   while (FN < a.F) FN *= 2;
   if (a.bf16) {
     switch (FN) {
-      case 32: run_conv<__nv_bfloat16, 32>(a, i, k, o, st); break;
-      case 64: run_conv<__nv_bfloat16, 64>(a, i, k, o, st); break;
-      case 128: run_conv<__nv_bfloat16, 128>(a, i, k, o, st); break;
-      default: run_conv<__nv_bfloat16, 256>(a, i, k, o, st); break;
+      case 32: run_conv<__nv_bfloat16, 32>(a, i, k, o, st, mk); break;
+      case 64: run_conv<__nv_bfloat16, 64>(a, i, k, o, st, mk); break;
+      case 128: run_conv<__nv_bfloat16, 128>(a, i, k, o, st, mk); break;
+      default: run_conv<__nv_bfloat16, 256>(a, i, k, o, st, mk); break;
     }
   } else {
     switch (FN) {
-      case 32: run_conv<float, 32>(a, i, k, o, st); break;
-      case 64: run_conv<float, 64>(a, i, k, o, st); break;
-      case 128: run_conv<float, 128>(a, i, k, o, st); break;
-      default: run_conv<float, 256>(a, i, k, o, st); break;
+      case 32: run_conv<float, 32>(a, i, k, o, st, mk); break;
+      case 64: run_conv<float, 64>(a, i, k, o, st, mk); break;
+      case 128: run_conv<float, 128>(a, i, k, o, st, mk); break;
+      default: run_conv<float, 256>(a, i, k, o, st, mk); break;
     }
   }
 }

@@ -40,6 +40,10 @@ struct Kernel {
   GemmTcArgs gemm;
   ConvTcArgs conv;
   int launches = 1;
+  std::vector<std::string> launch_names{"generic_simt"};
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  int marks_used = 0;
   std::string plan_info;
   void* ws = nullptr;  // family workspace
   // host-buffer execute staging (allocated on first use)
@@ -135,6 +139,7 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         const bool bf16 = k->variant == 3;
         if (op.kind == Kind::Gemm && gemm_tc_ok(op, bf16)) {
           k->family = Family::GemmTc;
+          k->launch_names = {"gemm_tc"};
           GemmTcArgs& g = k->gemm;
           g.M = static_cast<int>(op.param("M"));
           g.N = static_cast<int>(op.param("N"));
@@ -148,6 +153,7 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
           k->family = Family::ConvTc;
           k->launches = 3;
+          k->launch_names = {"nchw_to_nhwc", "weights_rsfc", "conv_tc"};
           ConvTcArgs& c = k->conv;
           c.N = static_cast<int>(op.param("N"));
           c.C = static_cast<int>(op.param("C"));
@@ -192,6 +198,8 @@ void destroy(Kernel* k) {
     if (p) cudaFree(p);
   if (k->d_out) cudaFree(k->d_out);
   if (k->ws) cudaFree(k->ws);
+  for (auto& e : k->ev)
+    if (e) cudaEventDestroy(e);
   delete k;
 }
 
@@ -213,18 +221,44 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
   for (int i = 0; i < n_in; ++i)
     if (!d_in[i]) throw Error(Code::ShapeMismatch, "null input pointer");
   auto st = static_cast<cudaStream_t>(stream);
+  Marks mk;
+  if (k->timing) mk.ev = k->ev;
   switch (k->family) {
     case Family::Generic:
+      mk.mark(st);
       launch_generic(k->gplan, k->f64, op.dtype_bytes == 2, d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out,
                      static_cast<int>(op.batch), st);
+      mk.mark(st);
       break;
     case Family::GemmTc:
+      mk.mark(st);
       launch_gemm_tc(k->gemm, d_in[0], d_in[1], d_out, st);
+      mk.mark(st);
       break;
     case Family::ConvTc:
-      launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st);
+      launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st, mk);
       break;
   }
+  k->marks_used = mk.next;
+}
+
+void set_timing(Kernel* k, bool on) {
+  if (on && !k->ev[0])
+    for (auto& e : k->ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+  k->timing = on;
+}
+
+std::vector<std::pair<std::string, float>> timings(Kernel* k) {
+  std::vector<std::pair<std::string, float>> out;
+  if (!k->timing || k->marks_used < 2) return out;
+  check_cuda(cudaEventSynchronize(k->ev[k->marks_used - 1]), "cudaEventSynchronize");
+  for (int i = 1; i < k->marks_used; ++i) {
+    float ms = 0.f;
+    check_cuda(cudaEventElapsedTime(&ms, k->ev[i - 1], k->ev[i]), "cudaEventElapsedTime");
+    const size_t j = static_cast<size_t>(i - 1);
+    out.emplace_back(j < k->launch_names.size() ? k->launch_names[j] : "launch", ms);
+  }
+  return out;
 }
 
 void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, void* stream) {

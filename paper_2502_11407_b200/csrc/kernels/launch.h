@@ -9,6 +9,16 @@
 
 namespace gb::dev {
 
+// Optional per-launch timing marks: when `ev` is non-null, ev[0] is recorded before the first
+// launch and ev[i] after the i-th launch of the family, all on the launch stream.
+struct Marks {
+  cudaEvent_t* ev = nullptr;
+  int next = 0;
+  void mark(cudaStream_t st) {
+    if (ev) cudaEventRecord(ev[next++], st);
+  }
+};
+
 // ---- state-driven SIMT family (generic.cu) ----
 int generic_max_width(bool f64);
 void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, const void* in1, void* out,
@@ -44,6 +54,6 @@ struct ConvTcArgs {
 };
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
-void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st);
+void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
 
 }  // namespace gb::dev

@@ -98,6 +98,8 @@ def _load() -> ctypes.CDLL:
         "gensor_execute_host": (I, [P, PP, I, P, P]),
         "gensor_kernel_free": (None, [P]),
         "gensor_launch_count": (ctypes.c_uint64, []),
+        "gensor_kernel_set_timing": (I, [P, I]),
+        "gensor_kernel_timings": (I, [P, ctypes.POINTER(ctypes.c_float), I, IP, ctypes.c_char_p, SZ]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -115,7 +117,7 @@ EXPORTED = [
     "gensor_candidates", "gensor_caching_benefit", "gensor_vthread_conflict_ratio",
     "gensor_anneal_cache_multiplier", "gensor_record_probability", "gensor_derive_seed",
     "gensor_kernel_prepare", "gensor_kernel_info", "gensor_execute", "gensor_execute_host",
-    "gensor_kernel_free", "gensor_launch_count",
+    "gensor_kernel_free", "gensor_launch_count", "gensor_kernel_set_timing", "gensor_kernel_timings",
 ]
 
 
@@ -379,6 +381,17 @@ class Kernel:
         ptrs = (ctypes.c_void_p * max(1, len(inputs)))(*[_ptr(t) for t in inputs])
         _check(_lib.gensor_execute_host(self._h, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
                                         ctypes.c_void_p(_stream(stream))))
+
+    def set_timing(self, on: bool = True) -> None:
+        _check(_lib.gensor_kernel_set_timing(self._h, 1 if on else 0))
+
+    def timings(self) -> list:
+        """[(launch name, ms)] of the last execute (CUDA events on the execute stream)."""
+        ms = (ctypes.c_float * 8)()
+        n = ctypes.c_int(0)
+        names = ctypes.create_string_buffer(4096)
+        _check(_lib.gensor_kernel_timings(self._h, ms, 8, ctypes.byref(n), names, len(names)))
+        return list(zip(json.loads(names.value.decode() or "[]"), list(ms)[: n.value]))
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
