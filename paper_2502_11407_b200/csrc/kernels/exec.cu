@@ -4,7 +4,9 @@
 #include <atomic>
 #include <cstring>
 #include <sstream>
+#include <cmath>
 #include <string>
+#include <vector>
 
 #include "../host/device.hpp"
 #include "../host/error.hpp"
@@ -28,7 +30,7 @@ void check_cuda(cudaError_t e, const char* what) {
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-enum class Family { Generic, GemmTc, ConvTc };
+enum class Family { Generic, GemmTc, ConvTc, Stream };
 
 struct Kernel {
   OpDesc op;
@@ -39,6 +41,7 @@ struct Kernel {
   bool f64 = false;
   GemmTcArgs gemm;
   ConvTcArgs conv;
+  StreamArgs stream;
   int launches = 1;
   std::vector<std::string> launch_names{"generic_simt"};
   bool timing = false;
@@ -63,6 +66,130 @@ int64_t pow2_clamp(int64_t v, int64_t lo, int64_t hi) {
   return p;
 }
 
+bool stream_ok(const OpDesc& op) {
+  if (op.dtype_bytes != 4 || op.batch != 1) return false;
+  switch (op.kind) {
+    case Kind::Gemv:
+    case Kind::Softmax:
+      return true;
+    case Kind::AvgPool2d:
+    case Kind::DwConv2d:
+      return op.ax[4].extent <= 8 && op.ax[5].extent <= 8;  // window axes (i,j / r,s)
+    default:
+      return false;
+  }
+}
+
+// Reduce-iteration order of one output under the interpreter's loop nest (SPEC.md:470-478 /
+// oracle_interpret): per level the reduce axes in axis order (radix T_{l-1}/T_l, step T_l), then
+// the scalar reduce loops (radix T_L, step 1); guarded (padded) iterations are skipped.
+void window_order(const OpDesc& op, const Sched& s, StreamWinArgs& w) {
+  int ra = -1, sa = -1;
+  for (int a = 0; a < op.naxes; ++a)
+    if (op.ax[a].reduce) (ra < 0 ? ra : sa) = a;
+  struct Loop {
+    int axis;
+    int64_t radix, step;
+  };
+  std::vector<Loop> loops;
+  const int L = s.L;
+  for (int l = 1; l <= L; ++l)
+    for (int a : {ra, sa}) loops.push_back({a, s.tile(op, a, l - 1) / s.tile(op, a, l), s.tile(op, a, l)});
+  for (int a : {ra, sa}) loops.push_back({a, L ? s.tile(op, a, L) : op.ax[a].padded, 1});
+  std::vector<int64_t> dig(loops.size(), 0);
+  w.n_order = 0;
+  for (;;) {
+    int64_t r = 0, c = 0;
+    for (size_t q = 0; q < loops.size(); ++q) (loops[q].axis == ra ? r : c) += dig[q] * loops[q].step;
+    if (r < w.R && c < w.S) w.order[w.n_order++] = static_cast<uint8_t>((r << 4) | c);
+    int q = static_cast<int>(loops.size()) - 1;
+    for (; q >= 0; --q) {
+      if (++dig[static_cast<size_t>(q)] < loops[static_cast<size_t>(q)].radix) break;
+      dig[static_cast<size_t>(q)] = 0;
+    }
+    if (q < 0) break;
+  }
+  bool rmajor = true, smajor = true;
+  for (int q = 0; q < w.n_order; ++q) {
+    const int r = w.order[q] >> 4, c = w.order[q] & 15;
+    rmajor &= (r * w.S + c) == q;
+    smajor &= (c * w.R + r) == q;
+  }
+  w.order_kind = rmajor ? 1 : (smajor ? 2 : 0);
+}
+
+// Stream plan from a complete schedule: the level-1 spatial tile is the CTA work unit.
+StreamArgs lower_stream(const OpDesc& op, const Sched& s, int sms) {
+  StreamArgs a;
+  a.sms = sms;
+  auto t1 = [&](int axis) { return s.L ? s.tile(op, axis, 1) : op.ax[axis].padded; };
+  if (op.kind == Kind::Gemv || op.kind == Kind::Softmax) {
+    a.kind = op.kind == Kind::Gemv ? StreamKind::Gemv : StreamKind::Softmax;
+    a.M = op.ax[0].extent;
+    a.N = op.ax[1].extent;
+    // gemv: a row is split over wpr warps so each warp keeps 8 x 128-bit loads in flight per lane
+    if (op.kind == Kind::Gemv) {
+      a.wpr = 1;
+      while (a.wpr < 8 && a.N / 4 >= static_cast<int64_t>(a.wpr) * 2 * 32 * 8) a.wpr *= 2;
+    }
+    const int64_t step = op.kind == Kind::Gemv ? 8 / a.wpr : 1;
+    // rows per unit: the level-1 m tile, halved while the grid would see fewer than 4 units per
+    // resident CTA slot (8 x 256-thread CTAs per SM), so the persistent CTAs finish together
+    int64_t rpu = std::max<int64_t>(step, t1(0));
+    const int64_t slots = static_cast<int64_t>(sms) * 8;
+    while (rpu > step && (a.M + rpu - 1) / rpu < 4 * slots) rpu = std::max<int64_t>(step, rpu / 2);
+    a.rows_per_unit = std::min<int64_t>(std::max<int64_t>(1, a.M), rpu);
+    return a;
+  }
+  a.kind = op.kind == Kind::AvgPool2d ? StreamKind::AvgPool : StreamKind::DwConv;
+  StreamWinArgs& w = a.win;
+  w.sms = sms;
+  // axes n c h w + window axes (pool i j / dw r s), op_spec.cpp:184-193
+  w.C = op.ax[1].extent;
+  w.planes = op.ax[0].extent * w.C;
+  w.H = op.param("H");
+  w.W = op.param("W");
+  w.OH = op.ax[2].extent;
+  w.OW = op.ax[3].extent;
+  w.R = static_cast<int32_t>(op.ax[4].extent);
+  w.S = static_cast<int32_t>(op.ax[5].extent);
+  w.stride = static_cast<int32_t>(op.stride);
+  w.divisor = op.kind == Kind::AvgPool2d ? w.R * w.S : 0;
+  window_order(op, s, w);
+  // band: the level-1 h tile (output rows), cut so one staging buffer stays <= 24 KB (3 CTAs of
+  // three buffers per SM) and rounded to the 4-row thread tile; among the legal band heights the
+  // one that keeps the CTA's warps fullest is taken.
+  const int h_axis = 2;
+  const int64_t want = std::min<int64_t>(t1(h_axis), w.OH);
+  const int64_t tiles_x = (w.OW + 3) / 4;
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t b = 1; b <= std::max<int64_t>(1, want); b = b < 4 ? b + 1 : b + 4) {
+    const int64_t rows = (b - 1) * w.stride + w.R;
+    if (((rows + 4 * w.stride) * w.W + 8) * 4 > 24 * 1024 && b > 1) break;
+    const int64_t tiles = tiles_x * ((b + 3) / 4);
+    const int64_t thr = std::min<int64_t>(256, (tiles + 31) / 32 * 32);
+    const double rounds = std::ceil(static_cast<double>(tiles) / thr);
+    const double eff = static_cast<double>(tiles) / (rounds * thr) + 1e-3 * static_cast<double>(b) / want;
+    if (eff >= best_eff) {
+      best_eff = eff;
+      best = b;
+    }
+  }
+  w.band_rows = static_cast<int32_t>(best);
+  w.in_rows = static_cast<int32_t>((best - 1) * w.stride + w.R);
+  w.bands = (w.OH + best - 1) / best;
+  w.units = w.planes * w.bands;
+  // staging buffer: the band's input rows plus slack so that partial edge tiles (rows rounded
+  // up to the 4-row thread tile, columns past OW) read inside the buffer; those reads only feed
+  // outputs that are never stored
+  const int64_t rows_rd = ((best + 3) / 4 * 4 - 1) * w.stride + w.R + 1;
+  w.buf_floats = (std::max<int64_t>(rows_rd, w.in_rows) * w.W + 4 + 3 * w.stride + 3) / 4 * 4;
+  const int64_t tiles = tiles_x * ((best + 3) / 4);
+  w.threads = static_cast<int32_t>(std::min<int64_t>(256, (tiles + 31) / 32 * 32));
+  return a;
+}
+
 bool gemm_tc_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Gemm) return false;
   if (bf16 != (op.dtype_bytes == 2)) return false;  // operands are read in their stored dtype
@@ -82,6 +209,7 @@ int resolve_variant(const OpDesc& op, int variant) {
   if (op.kind == Kind::Gemm && op.dtype_bytes == 2 && gemm_tc_ok(op, true)) return 3;
   if (op.kind == Kind::Gemm && gemm_tc_ok(op, false)) return 2;
   if (op.kind == Kind::Conv2d && conv_tc_ok(op, false)) return 2;
+  if (stream_ok(op)) return 4;
   return 1;
 }
 
@@ -180,6 +308,25 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         }
         break;
       }
+      case 4: {
+        if (!stream_ok(op))
+          throw Error(Code::Unsupported, std::string("stream not available for ") + op.label());
+        k->family = Family::Stream;
+        k->stream = lower_stream(op, s, sms);
+        const StreamArgs& a = k->stream;
+        static const char* names[] = {"gemv_stream", "softmax_stream", "avgpool_stream", "dwconv_stream"};
+        k->launch_names = {names[static_cast<int>(a.kind)]};
+        pi << "{\"family\":\"" << names[static_cast<int>(a.kind)] << "\"";
+        if (a.kind == StreamKind::Gemv || a.kind == StreamKind::Softmax)
+          pi << ",\"rows_per_unit\":" << a.rows_per_unit << ",\"warps_per_row\":" << a.wpr << ",\"units\":"
+             << (a.M + a.rows_per_unit - 1) / a.rows_per_unit << ",\"block\":256,\"grid\":\"persistent\"";
+        else
+          pi << ",\"band_rows\":" << a.win.band_rows << ",\"in_rows\":" << a.win.in_rows << ",\"units\":"
+             << a.win.units << ",\"block\":" << a.win.threads << ",\"thread_tile\":[4,4],\"order_kind\":"
+             << a.win.order_kind << ",\"smem_per_cta\":" << 3 * a.win.buf_floats * 4 << ",\"grid\":\"persistent\"";
+        pi << "}";
+        break;
+      }
       default:
         throw Error(Code::Unsupported, "variant " + std::to_string(variant) + " not available for " + op.label());
     }
@@ -237,6 +384,11 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
       break;
     case Family::ConvTc:
       launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st, mk);
+      break;
+    case Family::Stream:
+      mk.mark(st);
+      launch_stream(k->stream, d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out, st);
+      mk.mark(st);
       break;
   }
   k->marks_used = mk.next;

@@ -56,4 +56,34 @@ bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
 
+// ---- HBM-streaming family (stream.cu): gemv / softmax / avgpool2d / dwconv2d ----
+enum class StreamKind : int { Gemv, Softmax, AvgPool, DwConv };
+
+// Window ops: a unit is a band of `band_rows` output rows of one (n, c) plane; its input rows
+// [oh0*stride, oh0*stride + in_rows) are one contiguous range of the NCHW input.
+struct StreamWinArgs {
+  int64_t planes = 0;       // N * C
+  int64_t C = 1, H = 0, W = 0, OH = 0, OW = 0;
+  int32_t R = 1, S = 1, stride = 1, divisor = 0;  // divisor: F*F for avgpool, 0 for dwconv
+  int32_t band_rows = 1, in_rows = 1;
+  int64_t bands = 1, units = 0;
+  int64_t buf_floats = 0;   // one staging buffer (phase slack included), floats
+  int32_t threads = 256;
+  int32_t sms = 148;
+  int32_t vec = 0, vec_out = 0;  // set at launch from pointer alignment
+  int32_t order_kind = 0;   // interpreter reduce order: 1 r-major, 2 s-major, 0 other (list below)
+  int32_t n_order = 0;
+  uint8_t order[64];        // (r << 4) | s in the interpreter's accumulation order
+};
+
+struct StreamArgs {
+  StreamKind kind = StreamKind::Gemv;
+  int64_t M = 0, N = 0;       // gemv / softmax rows x cols
+  int64_t rows_per_unit = 1;  // gemv / softmax: rows per CTA work unit (level-1 m tile, split for balance)
+  int32_t wpr = 1;            // gemv: warps per row (1, 2, 4, 8)
+  int32_t sms = 148;
+  StreamWinArgs win;
+};
+void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* out, cudaStream_t st);
+
 }  // namespace gb::dev

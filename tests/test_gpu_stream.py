@@ -1,0 +1,220 @@
+"""GPU parity of the HBM-streaming family (variant "stream": gemv, softmax, avgpool2d, dwconv2d)
+against the CPU oracle (oracle/gensor_oracle.c).
+
+Bars:
+  * integer-valued inputs U{-2..2}: BIT-EXACT against interpret(lower(state)) rounded to fp32
+    (gemv, dwconv2d, avgpool2d; avgpool's fp32 sum is exact and its division correctly rounded);
+  * U(-1,1) inputs: max|gpu - oracle| <= STREAM_TOL * max|oracle| (normwise), gemv / window ops;
+  * softmax (extension op, parity unpinned by the reference): elementwise relative error
+    <= SOFTMAX_RTOL against the oracle's fp64 softmax.
+Window-op schedules cover the three accumulation orders the interpreter can produce for a 3x3
+window (r-major, s-major, interleaved), each hitting a different kernel path.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import B200_REF, GENERIC
+
+STREAM_TOL = 2e-6
+SOFTMAX_RTOL = 2e-6
+
+torch = pytest.importorskip("torch")
+g = pytest.importorskip("paper_2502_11407_b200")
+from oracle import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+OPS = [
+    {"kind": "gemv", "M": 100, "N": 64},
+    {"kind": "gemv", "M": 37, "N": 77},            # unaligned rows: scalar path
+    {"kind": "gemv", "M": 1, "N": 1},
+    {"kind": "gemv", "M": 513, "N": 4100},
+    {"kind": "avgpool2d", "I": [2, 5, 11, 10], "F": 3, "S": 1},
+    {"kind": "avgpool2d", "I": [2, 3, 17, 18], "F": 3, "S": 2},
+    {"kind": "avgpool2d", "I": [1, 3, 8, 8], "F": 2, "S": 2},
+    {"kind": "avgpool2d", "I": [2, 4, 9, 12], "F": 5, "S": 1},
+    {"kind": "avgpool2d", "I": [3, 8, 58, 58], "F": 3, "S": 1},
+    {"kind": "dwconv2d", "I": [2, 6, 10, 10], "K": [6, 1, 3, 3], "S": 1},
+    {"kind": "dwconv2d", "I": [2, 6, 19, 21], "K": [6, 1, 3, 3], "S": 2},
+    {"kind": "dwconv2d", "I": [1, 5, 12, 13], "K": [5, 1, 5, 5], "S": 1},
+    {"kind": "dwconv2d", "I": [2, 16, 114, 114], "K": [16, 1, 3, 3], "S": 1},
+]
+
+
+def _inputs(doc, rng, integer):
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    xs = []
+    for t in op.tensors[:-1]:
+        n = int(np.prod(t["true_dims"])) * op.batch
+        x = rng.integers(-2, 3, size=n) if integer else rng.uniform(-1, 1, size=n)
+        xs.append(x.astype(np.float32))
+    return op, xs
+
+
+def _run(op, sched, idx, xs, nout, variant="stream"):
+    k = g.Kernel(op, sched, idx, variant)
+    assert k.info["variant_name"] == variant
+    out = torch.full((nout,), float("nan"), dtype=torch.float32, device="cuda")
+    k.execute([torch.from_numpy(x).cuda() for x in xs], out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64), k
+
+
+def _schedules(op):
+    out = []
+    for prof in (GENERIC, B200_REF):
+        out.append(g.optimize(op, g.HardwareSpec.load_text(json.dumps(prof)), g.EngineConfig(seed=1, top_k=2)))
+    out.append(g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(seed=2, top_k=2, mode="b200")))
+    return out
+
+
+def _f32(ref):
+    return ref.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("doc", OPS, ids=lambda d: json.dumps(d))
+def test_stream_integer_bit_exact(doc):
+    rng = np.random.default_rng(0)
+    op, xs = _inputs(doc, rng, integer=True)
+    for sched in _schedules(op):
+        for i, res in enumerate(sched):
+            ref = _f32(O.interpret(doc, res["state"], xs))
+            got, _ = _run(op, sched, i, xs, ref.size)
+            assert np.array_equal(got, ref), (res["state"]["repr"], np.abs(got - ref).max())
+
+
+@pytest.mark.parametrize("doc", OPS, ids=lambda d: json.dumps(d))
+def test_stream_random_tolerance(doc):
+    rng = np.random.default_rng(1)
+    op, xs = _inputs(doc, rng, integer=False)
+    for sched in _schedules(op):
+        ref = O.interpret(doc, sched[0]["state"], xs)
+        got, _ = _run(op, sched, 0, xs, ref.size)
+        assert np.abs(got - ref).max() <= STREAM_TOL * max(1e-30, np.abs(ref).max()), sched[0]["state"]["repr"]
+
+
+# Accumulation orders of a 3x3 window under the interpreter's loop nest:
+#   r-major  i=[4,4] j=[4,4]  (lexicographic)          -> fast streamed-rows path
+#   s-major  i=[4,4] j=[2,1]  (j tiled, i scalar)       -> fast full-patch path
+#   mixed    i=[2,1] j=[2,1]  (tile digits interleave)  -> generic order-list path
+ORDER_TRACES = {
+    "r_major": [[3, -1, 0], [3, -1, 0]],
+    "s_major": [[0, 5, 2], [3, -1, 0], [0, 5, 2], [3, -1, 0]],
+    "mixed": [[0, 4, 2], [0, 5, 2], [3, -1, 0], [0, 4, 2], [0, 5, 2], [3, -1, 0]],
+}
+
+
+@pytest.mark.parametrize("order", sorted(ORDER_TRACES))
+@pytest.mark.parametrize("doc", [
+    {"kind": "avgpool2d", "I": [2, 3, 13, 14], "F": 3, "S": 1},
+    {"kind": "avgpool2d", "I": [2, 3, 13, 14], "F": 3, "S": 2},
+    {"kind": "dwconv2d", "I": [2, 3, 13, 14], "K": [3, 1, 3, 3], "S": 1},
+    {"kind": "dwconv2d", "I": [2, 3, 15, 12], "K": [3, 1, 3, 3], "S": 2},
+], ids=lambda d: json.dumps(d))
+def test_window_orders_bit_exact(doc, order):
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    hw = g.HardwareSpec.load_text(json.dumps(GENERIC))
+    sched = g.from_trace(op, hw, ORDER_TRACES[order])
+    rng = np.random.default_rng(2)
+    for integer in (True, False):
+        _, xs = _inputs(doc, rng, integer)
+        ref = _f32(O.interpret(doc, sched[0]["state"], xs))
+        got, k = _run(op, sched, 0, xs, ref.size)
+        assert k.info["plan"]["order_kind"] == {"r_major": 1, "s_major": 2, "mixed": 0}[order]
+        if integer or doc["kind"] == "dwconv2d":
+            # same fp32 operation sequence as the interpreter's order: dwconv matches to the
+            # rounding of fp32 FMAs vs fp64 sums; integer inputs exactly
+            tol = 0.0 if integer else STREAM_TOL * np.abs(ref).max()
+            assert np.abs(got - ref).max() <= tol
+        else:
+            assert np.abs(got - ref).max() <= STREAM_TOL * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("shape", [(64, 4096), (33, 1000), (17, 12000), (5, 7), (300, 128)])
+def test_softmax_parity(shape):
+    M, N = shape
+    doc = {"kind": "softmax", "M": M, "N": N}
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal(M * N) * 2.0).astype(np.float32)
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+    ref = O.reference_compute(doc, [x])
+    got, _ = _run(op, sched, 0, [x], ref.size)
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert rel.max() <= SOFTMAX_RTOL, rel.max()
+    assert np.allclose(got.reshape(M, N).sum(1), 1.0, atol=1e-5)
+
+
+def test_softmax_extreme_rows():
+    """Rows with huge spread, ties at the max, and constant rows."""
+    M, N = 4, 4096
+    x = np.zeros((M, N), np.float32)
+    x[0] = np.linspace(-100, 100, N)
+    x[1, ::2] = 50.0
+    x[2] = 3.0
+    x[3] = np.random.default_rng(4).uniform(-1e4, 1e4, N)
+    doc = {"kind": "softmax", "M": M, "N": N}
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+    ref = O.reference_compute(doc, [x.reshape(-1)])
+    got, _ = _run(op, sched, 0, [x.reshape(-1)], ref.size)
+    big = ref > 1e-30
+    assert np.all(np.abs(got[big] - ref[big]) <= SOFTMAX_RTOL * ref[big])
+    assert np.all(np.abs(got[~big]) <= 1e-30)
+
+
+# ---- BASELINE sizes (configs[3]): the oracle still finishes in seconds with OpenMP ---------
+def test_rowsum_full_size():
+    doc = {"kind": "gemv", "M": 32768, "N": 4096}
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+    a = torch.rand(32768 * 4096, device="cuda", generator=torch.Generator("cuda").manual_seed(0)) * 2 - 1
+    x = torch.ones(4096, device="cuda")
+    y = torch.empty(32768, device="cuda")
+    k = g.Kernel(op, sched, 0, "auto")
+    assert k.info["variant_name"] == "stream"
+    k.execute([a, x], y)
+    ref = O.reference_compute(doc, [a.cpu().numpy(), x.cpu().numpy()], threads=8)
+    got = y.cpu().numpy().astype(np.float64)
+    assert np.abs(got - ref).max() <= STREAM_TOL * np.abs(ref).max()
+    # integer property: row sums of integer matrices are exact
+    ai = torch.randint(-2, 3, (32768 * 4096,), device="cuda", dtype=torch.int32).float()
+    k.execute([ai, x], y)
+    exact = ai.view(32768, 4096).double().sum(1).float()
+    assert torch.equal(y.cpu(), exact.cpu())
+
+
+def test_softmax_full_size_rows_sum_to_one():
+    doc = {"kind": "softmax", "M": 32768, "N": 4096}
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+    x = torch.randn(32768 * 4096, device="cuda", generator=torch.Generator("cuda").manual_seed(1)) * 2
+    y = torch.empty_like(x)
+    g.Kernel(op, sched, 0, "auto").execute([x], y)
+    s = y.view(32768, 4096).double().sum(1)
+    assert torch.allclose(s, torch.ones_like(s), atol=1e-5)
+    # spot rows against the oracle
+    rows = [0, 12345, 32767]
+    sub = x.view(32768, 4096)[rows].cpu().numpy().reshape(-1)
+    ref = O.reference_compute({"kind": "softmax", "M": 3, "N": 4096}, [sub])
+    got = y.view(32768, 4096)[rows].cpu().numpy().reshape(-1).astype(np.float64)
+    assert (np.abs(got - ref) / ref).max() <= SOFTMAX_RTOL
+
+
+@pytest.mark.parametrize("kind", ["avgpool2d", "dwconv2d"])
+def test_window_full_size(kind):
+    doc = ({"kind": "avgpool2d", "I": [32, 256, 114, 114], "F": 3, "S": 1} if kind == "avgpool2d" else
+           {"kind": "dwconv2d", "I": [32, 256, 114, 114], "K": [256, 1, 3, 3], "S": 1})
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+    gen = torch.Generator("cuda").manual_seed(5)
+    xs = [torch.randint(-2, 3, (int(np.prod(t["true_dims"])),), device="cuda", generator=gen).float()
+          for t in op.tensors[:-1]]
+    out = torch.empty(int(np.prod(op.tensors[-1]["true_dims"])), device="cuda")
+    k = g.Kernel(op, sched, 0, "auto")
+    assert k.info["variant_name"] == "stream"
+    k.execute(xs, out)
+    ref = _f32(O.interpret(doc, sched[0]["state"], [x.cpu().numpy() for x in xs], threads=8))
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), ref)
