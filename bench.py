@@ -427,6 +427,7 @@ def run_ours(args):
                     "value": w / (statistics.mean(r["step_ms"]) / 1e3) / (1e12 if sp["unit"] == "TFLOP/s" else 1e9),
                     "unit": sp["unit"], "ms_per_step": statistics.mean(r["step_ms"]),
                     "roofline": roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname)),
+                    "launch_breakdown_ms": {n: statistics.mean(v) for n, v in r["launch_ms"].items()},
                     "construction_s": r["construct_s"],
                 }
                 del r
@@ -460,6 +461,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
                 "path": "gensor_execute_host (pinned host buffers)"},
         "gpu_launches": res["launches"],
+        "launch_breakdown_ms": {n: statistics.mean(v) for n, v in res["launch_ms"].items()},
         "construction_s": res["construct_s"],
         "construction_reference_s": ref_con,
         "clocks": clk.summary(),

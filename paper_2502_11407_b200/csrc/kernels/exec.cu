@@ -161,13 +161,13 @@ StreamArgs lower_stream(const OpDesc& op, const Sched& s, int sms) {
   // one that keeps the CTA's warps fullest is taken.
   const int h_axis = 2;
   const int64_t want = std::min<int64_t>(t1(h_axis), w.OH);
-  const int64_t tiles_x = (w.OW + 3) / 4;
+  const int64_t tiles_x = (w.OW + kWinTW - 1) / kWinTW;
   int64_t best = 1;
   double best_eff = -1.0;
-  for (int64_t b = 1; b <= std::max<int64_t>(1, want); b = b < 4 ? b + 1 : b + 4) {
-    const int64_t rows = (b - 1) * w.stride + w.R;
-    if (((rows + 4 * w.stride) * w.W + 8) * 4 > 24 * 1024 && b > 1) break;
-    const int64_t tiles = tiles_x * ((b + 3) / 4);
+  for (int64_t b = 1; b <= std::max<int64_t>(1, want); b = b < kWinTH ? b + 1 : b + kWinTH) {
+    const int64_t rows = ((b + kWinTH - 1) / kWinTH * kWinTH - 1) * w.stride + w.R + 1;
+    if ((rows * w.W + 8) * 4 > 24 * 1024 && b > 1) break;
+    const int64_t tiles = tiles_x * ((b + kWinTH - 1) / kWinTH);
     const int64_t thr = std::min<int64_t>(256, (tiles + 31) / 32 * 32);
     const double rounds = std::ceil(static_cast<double>(tiles) / thr);
     const double eff = static_cast<double>(tiles) / (rounds * thr) + 1e-3 * static_cast<double>(b) / want;
@@ -181,11 +181,11 @@ StreamArgs lower_stream(const OpDesc& op, const Sched& s, int sms) {
   w.bands = (w.OH + best - 1) / best;
   w.units = w.planes * w.bands;
   // staging buffer: the band's input rows plus slack so that partial edge tiles (rows rounded
-  // up to the 4-row thread tile, columns past OW) read inside the buffer; those reads only feed
+  // up to the thread tile, columns past OW) read inside the buffer; those reads only feed
   // outputs that are never stored
-  const int64_t rows_rd = ((best + 3) / 4 * 4 - 1) * w.stride + w.R + 1;
-  w.buf_floats = (std::max<int64_t>(rows_rd, w.in_rows) * w.W + 4 + 3 * w.stride + 3) / 4 * 4;
-  const int64_t tiles = tiles_x * ((best + 3) / 4);
+  const int64_t rows_rd = ((best + kWinTH - 1) / kWinTH * kWinTH - 1) * w.stride + w.R + 1;
+  w.buf_floats = (std::max<int64_t>(rows_rd, w.in_rows) * w.W + 4 + kWinTW * w.stride + 3) / 4 * 4;
+  const int64_t tiles = tiles_x * ((best + kWinTH - 1) / kWinTH);
   w.threads = static_cast<int32_t>(std::min<int64_t>(256, (tiles + 31) / 32 * 32));
   return a;
 }
@@ -322,7 +322,7 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
              << (a.M + a.rows_per_unit - 1) / a.rows_per_unit << ",\"block\":256,\"grid\":\"persistent\"";
         else
           pi << ",\"band_rows\":" << a.win.band_rows << ",\"in_rows\":" << a.win.in_rows << ",\"units\":"
-             << a.win.units << ",\"block\":" << a.win.threads << ",\"thread_tile\":[4,4],\"order_kind\":"
+             << a.win.units << ",\"block\":" << a.win.threads << ",\"thread_tile\":[" << kWinTH << "," << kWinTW << "],\"order_kind\":"
              << a.win.order_kind << ",\"smem_per_cta\":" << 3 * a.win.buf_floats * 4 << ",\"grid\":\"persistent\"";
         pi << "}";
         break;

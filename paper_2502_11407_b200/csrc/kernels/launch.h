@@ -58,6 +58,7 @@ void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaSt
 
 // ---- HBM-streaming family (stream.cu): gemv / softmax / avgpool2d / dwconv2d ----
 enum class StreamKind : int { Gemv, Softmax, AvgPool, DwConv };
+constexpr int kWinTH = 8, kWinTW = 2;  // window ops: outputs per thread (rows x cols)
 
 // Window ops: a unit is a band of `band_rows` output rows of one (n, c) plane; its input rows
 // [oh0*stride, oh0*stride + in_rows) are one contiguous range of the NCHW input.

@@ -169,9 +169,11 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(const float* __restrict__
 }
 
 // TMA-bulk gemv: CTA b owns a contiguous range of row units; a producer warp streams one row per
-// stage (cp.async.bulk, mbarrier transaction counts) into a ring of `stages` row buffers; the 8
-// consumer warps reduce each row against x (staged once in shared memory), post per-warp fp64
-// partials, and the producer adds them in fixed warp order when it recycles the stage.
+// stage (cp.async.bulk, mbarrier transaction counts) into a ring of `stages` (a multiple of 8) row
+// buffers; consumer
+// warp w reduces rows i = w (mod 8) of the range against x (staged once in shared memory) — 8 rows
+// in flight per CTA, each reduced by one warp in a fixed order (deterministic) — and releases the
+// stage as soon as its row is done.
 constexpr int kGemvBulkConsumers = 8;
 
 __global__ void __launch_bounds__(32 * (kGemvBulkConsumers + 1), 1)
@@ -184,7 +186,6 @@ __global__ void __launch_bounds__(32 * (kGemvBulkConsumers + 1), 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<int64_t>(stages) * N);
   uint64_t* empty = full + stages;
   uint64_t* xbar = empty + stages;
-  double* red = reinterpret_cast<double*>(xbar + 1);  // [stages][consumers]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
   const int64_t r0 = min(M, u0 * rows_per_unit), r1 = min(M, u1 * rows_per_unit);
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(32 * (kGemvBulkConsumers + 1), 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       tc::mbar_init(&full[i], 1);
-      tc::mbar_init(&empty[i], kGemvBulkConsumers);
+      tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(xbar, 1);
     tc::fence_barrier_init();
@@ -202,20 +203,11 @@ __global__ void __launch_bounds__(32 * (kGemvBulkConsumers + 1), 1)
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(xbar, row_bytes);
       bulk_g2s(xs, x, row_bytes, xbar);
-      for (int64_t i = 0; i < rows + stages; ++i) {
+      for (int64_t i = 0; i < rows; ++i) {
         const int st = static_cast<int>(i % stages);
-        const uint32_t ph = static_cast<uint32_t>((i / stages) & 1);
-        if (i >= stages) {  // stage st held row i - stages: finish it
-          tc::mbar_wait(&empty[st], ph ^ 1);
-          double t = 0.0;
-#pragma unroll
-          for (int w = 0; w < kGemvBulkConsumers; ++w) t += red[st * kGemvBulkConsumers + w];
-          y[r0 + i - stages] = static_cast<float>(t);
-        }
-        if (i < rows) {
-          tc::mbar_arrive_expect_tx(&full[st], row_bytes);
-          bulk_g2s(ring + static_cast<int64_t>(st) * N, A + (r0 + i) * N, row_bytes, &full[st]);
-        }
+        if (i >= stages) tc::mbar_wait(&empty[st], static_cast<uint32_t>(((i / stages) & 1) ^ 1));
+        tc::mbar_arrive_expect_tx(&full[st], row_bytes);
+        bulk_g2s(ring + static_cast<int64_t>(st) * N, A + (r0 + i) * N, row_bytes, &full[st]);
       }
     }
     return;
@@ -223,36 +215,35 @@ __global__ void __launch_bounds__(32 * (kGemvBulkConsumers + 1), 1)
   tc::mbar_wait(xbar, 0);
   const int64_t nv = N >> 2;
   const float4* xv = reinterpret_cast<const float4*>(xs);
-  for (int64_t i = 0; i < rows; ++i) {
+  for (int64_t i = warp; i < rows; i += kGemvBulkConsumers) {
     const int st = static_cast<int>(i % stages);
     tc::mbar_wait(&full[st], static_cast<uint32_t>((i / stages) & 1));
     const float4* rv = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(st) * N);
-    float p0 = 0.0f, p1 = 0.0f;
-    int64_t j = threadIdx.x;
-    for (; j + 32 * kGemvBulkConsumers < nv; j += 2 * 32 * kGemvBulkConsumers) {
+    // 4 independent fp32 FMA chains per lane, combined in fp64
+    float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int64_t j = lane;
+    for (; j + 3 * 32 < nv; j += 4 * 32) {
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const float4 a = rv[j + d * 32], b = xv[j + d * 32];
+        p[d] = fmaf(a.x, b.x, p[d]);
+        p[d] = fmaf(a.y, b.y, p[d]);
+        p[d] = fmaf(a.z, b.z, p[d]);
+        p[d] = fmaf(a.w, b.w, p[d]);
+      }
+    }
+    for (; j < nv; j += 32) {
       const float4 a = rv[j], b = xv[j];
-      const float4 c = rv[j + 32 * kGemvBulkConsumers], d = xv[j + 32 * kGemvBulkConsumers];
-      p0 = fmaf(a.x, b.x, p0);
-      p0 = fmaf(a.y, b.y, p0);
-      p0 = fmaf(a.z, b.z, p0);
-      p0 = fmaf(a.w, b.w, p0);
-      p1 = fmaf(c.x, d.x, p1);
-      p1 = fmaf(c.y, d.y, p1);
-      p1 = fmaf(c.z, d.z, p1);
-      p1 = fmaf(c.w, d.w, p1);
+      p[0] = fmaf(a.x, b.x, p[0]);
+      p[0] = fmaf(a.y, b.y, p[0]);
+      p[0] = fmaf(a.z, b.z, p[0]);
+      p[0] = fmaf(a.w, b.w, p[0]);
     }
-    if (j < nv) {
-      const float4 a = rv[j], b = xv[j];
-      p0 = fmaf(a.x, b.x, p0);
-      p0 = fmaf(a.y, b.y, p0);
-      p0 = fmaf(a.z, b.z, p0);
-      p0 = fmaf(a.w, b.w, p0);
-    }
-    const double v = warp_sum(static_cast<double>(p0) + static_cast<double>(p1));
-    if (lane == 0) {
-      red[st * kGemvBulkConsumers + warp] = v;
-      tc::mbar_arrive(&empty[st]);
-    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&empty[st]);  // the row is in registers: free the stage
+    const double v = warp_sum((static_cast<double>(p[0]) + static_cast<double>(p[1])) +
+                              (static_cast<double>(p[2]) + static_cast<double>(p[3])));
+    if (lane == 0) y[r0 + i] = static_cast<float>(v);
   }
 }
 
@@ -363,7 +354,9 @@ __global__ void __launch_bounds__(kSoftmaxThreads) k_softmax_any(const float* __
 }
 
 // ---- window ops: avgpool2d / dwconv2d --------------------------------------------------------
-constexpr int kTH = 4, kTW = 4;  // outputs per thread (rows x cols)
+// outputs per thread: a column strip of kTH rows (launch.h); adjacent lanes own adjacent columns,
+// so every shared-memory read of a warp is conflict-free (stride 1)
+constexpr int kTH = kWinTH, kTW = kWinTW;
 constexpr int kWinStages = 3;   // band staging buffers per CTA
 
 // Band geometry of unit u. Plane/row offsets stay 64-bit; everything inside a band is 32-bit.
@@ -407,94 +400,82 @@ __device__ __forceinline__ void issue_band(const StreamWinArgs& a, const float* 
   }
 }
 
+// Correctly rounded acc / F^2 (the oracle divides the window sum by the true F^2,
+// oracle_interpret): Markstein's sequence q0 = acc*y, r = acc - F^2*q0 (exact by FMA),
+// q = q0 + r*y with y = RN(1/F^2) is correctly rounded for normal results (checked against exact
+// rational division for F^2 in {9, 25, 49}); tiny / non-finite sums take the IEEE division.
+__device__ __forceinline__ float div_window(float acc, float d, float y) {
+  const float q0 = acc * y;
+  const float r = fmaf(-q0, d, acc);
+  const float q = fmaf(r, y, q0);
+  return (fabsf(acc) > 1e-30f && fabsf(acc) < 1e30f) ? q : __fdiv_rn(acc, d);
+}
+
 template <bool DW>
 __device__ __forceinline__ void store_row(const StreamWinArgs& a, float* orow, int ox, const float (&acc)[kTW]) {
   float o[kTW];
+  const float d = static_cast<float>(a.divisor), y = 1.0f / d;
 #pragma unroll
-  for (int j = 0; j < kTW; ++j) o[j] = DW ? acc[j] : __fdiv_rn(acc[j], static_cast<float>(a.divisor));
-  if (a.vec_out && ox + kTW <= a.OW) {
-    st_stream4(orow, make_float4(o[0], o[1], o[2], o[3]));
-  } else {
-#pragma unroll
-    for (int j = 0; j < kTW; ++j)
-      if (ox + j < a.OW) orow[j] = o[j];
-  }
-}
-
-// 3x3 window, reduce order r-major (the interpreter's lexicographic order): input rows of the
-// patch are streamed top to bottom; row y adds its r = y - i*STRIDE taps to output row i, so
-// every output sees r ascending and, within a row, s ascending — the oracle's order.
-template <bool DW, int STRIDE>
-__device__ __forceinline__ void tile3x3_rmajor(const StreamWinArgs& a, const float* band, const float (&w)[9],
-                                               float* __restrict__ out_band, int oy, int ox, int rows_out) {
-  constexpr int PH = (kTH - 1) * STRIDE + 3, PW = (kTW - 1) * STRIDE + 3;
-  const int W = static_cast<int>(a.W);
-  const float* src = band + (oy * STRIDE) * W + ox * STRIDE;
-  float acc[kTH][kTW];
-#pragma unroll
-  for (int i = 0; i < kTH; ++i)
-#pragma unroll
-    for (int j = 0; j < kTW; ++j) acc[i][j] = 0.0f;
-#pragma unroll
-  for (int y = 0; y < PH; ++y) {
-    float row[PW];
-#pragma unroll
-    for (int x = 0; x < PW; ++x) row[x] = src[y * W + x];
-#pragma unroll
-    for (int i = 0; i < kTH; ++i) {
-      const int r = y - i * STRIDE;
-      if (r < 0 || r > 2) continue;  // compile-time after unrolling
-#pragma unroll
-      for (int sx = 0; sx < 3; ++sx)
-#pragma unroll
-        for (int j = 0; j < kTW; ++j) {
-          const float v = row[j * STRIDE + sx];
-          if constexpr (DW)
-            acc[i][j] = fmaf(v, w[r * 3 + sx], acc[i][j]);
-          else
-            acc[i][j] += v;
-        }
+  for (int j = 0; j < kTW; ++j) o[j] = DW ? acc[j] : div_window(acc[j], d, y);
+  if constexpr (kTW == 2) {
+    if (a.vec_out && ox + 2 <= a.OW) {
+      __stcs(reinterpret_cast<float2*>(orow), make_float2(o[0], o[1]));
+      return;
     }
   }
-  const int OW = static_cast<int>(a.OW);
 #pragma unroll
-  for (int i = 0; i < kTH; ++i) {
-    if (oy + i >= rows_out) break;
-    store_row<DW>(a, out_band + (oy + i) * OW + ox, ox, acc[i]);
-  }
+  for (int j = 0; j < kTW; ++j)
+    if (ox + j < a.OW) __stcs(orow + j, o[j]);
 }
 
-// 3x3 window, reduce order s-major (s outer, r inner): the whole register patch is needed.
-template <bool DW, int STRIDE>
-__device__ __forceinline__ void tile3x3_smajor(const StreamWinArgs& a, const float* band, const float (&w)[9],
-                                               float* __restrict__ out_band, int oy, int ox, int rows_out) {
+// 3x3 window fast path. The (kTH-1)*STRIDE+3 x (kTW-1)*STRIDE+3 input patch is loaded into
+// registers first (independent shared loads, 64-bit pairs when rows are 8 B aligned), then every
+// output accumulates its 9 taps in the interpreter's order — r-major (r outer, s inner: the
+// lexicographic order) or s-major — with the kTH*kTW outputs as independent FMA chains.
+template <bool DW, int STRIDE, bool SMAJOR>
+__device__ __forceinline__ void tile3x3(const StreamWinArgs& a, const float* band, bool pairs, const float (&w)[9],
+                                        float* __restrict__ out_band, int oy, int ox, int rows_out) {
   constexpr int PH = (kTH - 1) * STRIDE + 3, PW = (kTW - 1) * STRIDE + 3;
   const int W = static_cast<int>(a.W);
   const float* src = band + (oy * STRIDE) * W + ox * STRIDE;
   float p[PH][PW];
+  if (pairs) {  // src is 8 B aligned on every row
 #pragma unroll
-  for (int y = 0; y < PH; ++y)
+    for (int y = 0; y < PH; ++y) {
 #pragma unroll
-    for (int x = 0; x < PW; ++x) p[y][x] = src[y * W + x];
+      for (int x = 0; x + 1 < PW; x += 2) {
+        const float2 v = *reinterpret_cast<const float2*>(src + y * W + x);
+        p[y][x] = v.x;
+        p[y][x + 1] = v.y;
+      }
+      if constexpr (PW % 2) p[y][PW - 1] = src[y * W + PW - 1];
+    }
+  } else {
+#pragma unroll
+    for (int y = 0; y < PH; ++y)
+#pragma unroll
+      for (int x = 0; x < PW; ++x) p[y][x] = src[y * W + x];
+  }
   float acc[kTH][kTW];
 #pragma unroll
   for (int i = 0; i < kTH; ++i)
 #pragma unroll
     for (int j = 0; j < kTW; ++j) acc[i][j] = 0.0f;
 #pragma unroll
-  for (int sx = 0; sx < 3; ++sx)
+  for (int q = 0; q < 9; ++q) {
+    const int r = SMAJOR ? q % 3 : q / 3;
+    const int sx = SMAJOR ? q / 3 : q % 3;
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < kTH; ++i)
 #pragma unroll
-      for (int i = 0; i < kTH; ++i)
-#pragma unroll
-        for (int j = 0; j < kTW; ++j) {
-          const float v = p[i * STRIDE + r][j * STRIDE + sx];
-          if constexpr (DW)
-            acc[i][j] = fmaf(v, w[r * 3 + sx], acc[i][j]);
-          else
-            acc[i][j] += v;
-        }
+      for (int j = 0; j < kTW; ++j) {
+        const float v = p[i * STRIDE + r][j * STRIDE + sx];
+        if constexpr (DW)
+          acc[i][j] = fmaf(v, w[r * 3 + sx], acc[i][j]);
+        else
+          acc[i][j] += v;
+      }
+  }
   const int OW = static_cast<int>(a.OW);
 #pragma unroll
   for (int i = 0; i < kTH; ++i) {
@@ -557,6 +538,7 @@ __global__ void __launch_bounds__(256) k_window(const StreamWinArgs a, const flo
     // rows past the plane's last output row belong to no output of this band
     const int rows_out = min(a.band_rows, static_cast<int32_t>(a.OH) - b.oh0);
     const float* band = sm + cur * a.buf_floats + b.ph;
+    const bool pairs = (a.W % 2 == 0) && (b.ph % 2 == 0);  // 8 B aligned patch rows (ox*STRIDE even)
     float* out_band = out + b.out0;
     const int c = static_cast<int>(b.plane % a.C);
     float w[9];
@@ -567,10 +549,10 @@ __global__ void __launch_bounds__(256) k_window(const StreamWinArgs a, const flo
     for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
       const int oy = (t / tiles_x) * kTH, ox = (t % tiles_x) * kTW;
       if (oy >= rows_out) continue;
-      if constexpr (MODE == 1) tile3x3_rmajor<DW, 1>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 2) tile3x3_smajor<DW, 1>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 3) tile3x3_rmajor<DW, 2>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 4) tile3x3_smajor<DW, 2>(a, band, w, out_band, oy, ox, rows_out);
+      if constexpr (MODE == 1) tile3x3<DW, 1, false>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 2) tile3x3<DW, 1, true>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 3) tile3x3<DW, 2, false>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 4) tile3x3<DW, 2, true>(a, band, pairs, w, out_band, oy, ox, rows_out);
       else tile_generic<DW>(a, band, DW ? wts + static_cast<int64_t>(c) * a.R * a.S : nullptr, out_band, oy, ox, rows_out);
     }
     __syncthreads();  // this buffer is refilled next iteration
@@ -631,6 +613,7 @@ __global__ void __launch_bounds__(288) k_window_bulk(const StreamWinArgs a, cons
     const Band b = band_of(a, u);
     const int rows_out = min(a.band_rows, static_cast<int32_t>(a.OH) - b.oh0);
     const float* band = sm + st * a.buf_floats + b.ph;
+    const bool pairs = (a.W % 2 == 0) && (b.ph % 2 == 0);  // 8 B aligned patch rows (ox*STRIDE even)
     float* out_band = out + b.out0;
     const int c = static_cast<int>(b.plane % a.C);
     float w[9];
@@ -641,10 +624,10 @@ __global__ void __launch_bounds__(288) k_window_bulk(const StreamWinArgs a, cons
     for (int t = threadIdx.x; t < tiles; t += consumers) {
       const int oy = (t / tiles_x) * kTH, ox = (t % tiles_x) * kTW;
       if (oy >= rows_out) continue;
-      if constexpr (MODE == 1) tile3x3_rmajor<DW, 1>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 2) tile3x3_smajor<DW, 1>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 3) tile3x3_rmajor<DW, 2>(a, band, w, out_band, oy, ox, rows_out);
-      else if constexpr (MODE == 4) tile3x3_smajor<DW, 2>(a, band, w, out_band, oy, ox, rows_out);
+      if constexpr (MODE == 1) tile3x3<DW, 1, false>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 2) tile3x3<DW, 1, true>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 3) tile3x3<DW, 2, false>(a, band, pairs, w, out_band, oy, ox, rows_out);
+      else if constexpr (MODE == 4) tile3x3<DW, 2, true>(a, band, pairs, w, out_band, oy, ox, rows_out);
       else tile_generic<DW>(a, band, DW ? wts + static_cast<int64_t>(c) * a.R * a.S : nullptr, out_band, oy, ox, rows_out);
     }
     __syncwarp();
@@ -704,10 +687,13 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
                                                                    a.rows_per_unit, units, a.wpr);
       };
       const size_t row_bytes = static_cast<size_t>(a.N) * 4;
-      const size_t budget = 200 * 1024;  // x + ring + per stage (2 barriers + 8 fp64 partials)
-      const int stages = static_cast<int>(std::min<size_t>(16, (budget - std::min(budget, row_bytes + 16)) / (row_bytes + 80)));
-      if (vec && a.N >= 256 && stages >= 3) {
-        const size_t smem = row_bytes * (stages + 1) + static_cast<size_t>(stages) * 80 + 16;
+      const size_t budget = 200 * 1024;  // x + ring + 2 barriers per stage
+      // stages: a multiple of the 8 consumer warps, so stage s is always consumed by warp s % 8 and
+      // a warp never waits on a fill more than one mbarrier phase ahead of the last one it consumed
+      int stages = static_cast<int>(std::min<size_t>(16, (budget - std::min(budget, row_bytes + 16)) / (row_bytes + 16)));
+      stages = stages / kGemvBulkConsumers * kGemvBulkConsumers;
+      if (vec && a.N >= 256 && stages >= kGemvBulkConsumers) {
+        const size_t smem = row_bytes * (stages + 1) + static_cast<size_t>(stages) * 16 + 16;
         check_cuda(cudaFuncSetAttribute(k_gemv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                    "gemv smem attribute");
         const int64_t grid = std::min<int64_t>(units, a.sms);
@@ -747,7 +733,7 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
     case StreamKind::DwConv: {
       StreamWinArgs w = a.win;
       w.vec = reinterpret_cast<uintptr_t>(in0) % 16 == 0;
-      w.vec_out = (w.OW % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+      w.vec_out = (w.OW % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 8 == 0);
       const bool dw = a.kind == StreamKind::DwConv;
       int mode = 0;
       if (w.R == 3 && w.S == 3 && (w.stride == 1 || w.stride == 2) && w.order_kind != 0)

@@ -31,6 +31,7 @@ OPS = [
     {"kind": "gemv", "M": 37, "N": 77},            # unaligned rows: scalar path
     {"kind": "gemv", "M": 1, "N": 1},
     {"kind": "gemv", "M": 513, "N": 4100},
+    {"kind": "gemv", "M": 4000, "N": 1024},       # many rows per CTA: the TMA ring wraps
     {"kind": "avgpool2d", "I": [2, 5, 11, 10], "F": 3, "S": 1},
     {"kind": "avgpool2d", "I": [2, 3, 17, 18], "F": 3, "S": 2},
     {"kind": "avgpool2d", "I": [1, 3, 8, 8], "F": 2, "S": 2},
