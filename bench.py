@@ -365,6 +365,130 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------
+SEQUENCE_NAMES = {"resnet50": "End-to-end ResNet-50 operator sequence (53 convs + pools + fc, global batch 128)",
+                  "gpt2": "End-to-end GPT-2 small operator sequence (12 layers + LM head, global batch 16 x 512)"}
+
+
+def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
+    """configs[4]: every op of the batch-sharded sequence constructed once (per distinct spec) and
+    executed in order each step. e2e: the shard's input batch H2D + the final output D2H around
+    the same on-device sequence (weights and intermediates stay resident)."""
+    from paper_2502_11407_b200 import sequences as S
+
+    seq = S.sharded(name, ws)
+    kern, bufs, con = {}, {}, {}
+    gen = torch.Generator(device=device)
+    gen.manual_seed(0)
+    for key, spec_op in S.distinct(seq).items():
+        op = g.TensorOpSpec.parse_text(json.dumps(spec_op))
+        t0 = time.perf_counter()
+        sched = g.optimize(op, hw, g.EngineConfig(seed=0, mode="b200"))
+        con[key] = time.perf_counter() - t0
+        k = g.Kernel(op, sched, 0, "auto")
+        xs, out = make_inputs(op, {"op": spec_op}, gen, torch, device)
+        kern[key] = (op, k)
+        bufs[key] = (xs, out)
+    keys = [json.dumps(sp, sort_keys=True) for _, sp in seq]
+    stream = torch.cuda.current_stream(device)
+
+    def step():
+        for key in keys:
+            kern[key][1].execute(bufs[key][0], bufs[key][1], stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(device)
+    # per-op breakdown (one extra pass, events between ops)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(keys) + 1)]
+    ev[0].record(stream)
+    for i, key in enumerate(keys):
+        kern[key][1].execute(bufs[key][0], bufs[key][1], stream)
+        ev[i + 1].record(stream)
+    ev[-1].synchronize()
+    per_op = {}
+    for i, (opname, _) in enumerate(seq):
+        key = keys[i]
+        ms = ev[i].elapsed_time(ev[i + 1])
+        kind = opname.split(".")[-1] if name == "gpt2" else ("conv" if "conv" in opname or "downsample" in opname else opname)
+        d = per_op.setdefault(kind, {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "n": 0,
+                                     "variant": kern[key][1].info["variant_name"]})
+        d["ms"] += ms
+        d["flops"] += kern[key][0].flops
+        d["bytes"] += kern[key][0].bytes
+        d["n"] += 1
+    n0 = g.launch_count()
+    step_ms = []
+    for _ in range(steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        step()
+        e.record(stream)
+        e.synchronize()
+        step_ms.append(s.elapsed_time(e))
+    launches = g.launch_count() - n0
+    flops = sum(kern[k][0].flops for k in keys)
+    # e2e: the shard's input batch from pinned host memory, the final output back
+    first, last = keys[0], keys[-1]
+    hin = bufs[first][0][0].cpu().pin_memory()
+    hout = torch.empty(bufs[last][1].numel(), dtype=bufs[last][1].dtype).pin_memory()
+    e2e_ms = []
+    for _ in range(max(3, steps // 2)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        bufs[first][0][0].copy_(hin, non_blocking=True)
+        step()
+        hout.copy_(bufs[last][1], non_blocking=True)
+        e.record(stream)
+        e.synchronize()
+        e2e_ms.append(s.elapsed_time(e))
+    return dict(seq=seq, step_ms=step_ms, e2e_ms=e2e_ms, per_op=per_op, launches=launches, flops=flops,
+                construct_s=sum(con.values()), n_distinct=len(con), h2d=hin.numel() * hin.element_size(),
+                d2h=hout.numel() * hout.element_size())
+
+
+def sequence_line(args, res, ws, peaks, tf32, clk, total_ms, e2e_ms):
+    ms_step = total_ms / args.steps
+    value = ws * res["flops"] / (ms_step / 1e3) / 1e12
+    e2e_value = ws * res["flops"] / (e2e_ms / 1e3) / 1e12
+    per_op = {}
+    for kind, d in res["per_op"].items():
+        per_op[kind] = {"n": d["n"], "ms": d["ms"], "share": d["ms"] / sum(x["ms"] for x in res["per_op"].values()),
+                        "tflops": d["flops"] / (d["ms"] / 1e3) / 1e12, "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                        "variant": d["variant"]}
+    top = max(per_op.items(), key=lambda kv: kv[1]["ms"])
+    d = res["per_op"][top[0]]
+    variant = d["variant"]
+    if variant in ("stream",):
+        ach, peak, unit, bound = d["bytes"] / (d["ms"] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s", "hbm"
+        src = f"hbm copy, {peaks['source']}"
+    else:
+        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        peak = tf32 if variant == "tc_tf32" else peaks["bf16_tflops"]
+        src = "cuBLAS tf32 8192^3 measured in this run" if variant == "tc_tf32" else f"bf16 dense, {peaks['source']}"
+        unit, bound = "TFLOP/s", "tensor"
+    dt = {"resnet50": "tf32 convs / fp32 pools (fp32 storage)", "gpt2": "bf16 GEMMs (fp32 accumulate), fp32 softmax"}
+    return {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dt[args.workload], "data": "synthetic U(-1,1)",
+        "config": {"workload": SEQUENCE_NAMES[args.workload], "ops": len(res["seq"]),
+                   "distinct_ops": res["n_distinct"],
+                   "parallelism": f"batch-sharded over {ws} GPU(s), one process per GPU, no collective",
+                   "l2": "flushed between steps (256 MiB write outside the events)"},
+        "roofline": {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                     "traffic": None, "kernel": f"{top[0]} ({variant})", "peak_source": src,
+                     "share_of_step": top[1]["share"]},
+        "per_op": per_op,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
+                "path": "input batch H2D + on-device sequence + final output D2H"},
+        "gpu_launches": res["launches"], "construction_s": res["construct_s"], "clocks": clk.summary(),
+        "cpu_baseline": None,
+    }
+
+
 def run_ours(args):
     import torch
 
@@ -384,13 +508,29 @@ def run_ours(args):
     tf32 = tf32_peak(torch, device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # 2x L2: flushed between steps
 
-    spec = WORKLOADS[args.workload]
-
     def barrier():
         torch.cuda.synchronize(device)
         if pg:
             pg.barrier()
         torch.cuda.synchronize(device)
+
+    if args.workload in SEQUENCE_NAMES:
+        barrier()
+        with ClockSampler(local) as clk:
+            res = run_sequence(g, torch, args.workload, hw, args.steps, args.warmup, device, ws, flush)
+        barrier()
+        total_ms, e2e_ms = sum(res["step_ms"]), statistics.mean(res["e2e_ms"])
+        if pg:
+            t = torch.tensor([total_ms, e2e_ms], device=device, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            total_ms, e2e_ms = t.tolist()
+        if rank == 0:
+            print(json.dumps(sequence_line(args, res, ws, peaks, tf32, clk, total_ms, e2e_ms)), flush=True)
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    spec = WORKLOADS[args.workload]
 
     barrier()
     with ClockSampler(local) as clk:
@@ -479,7 +619,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="conv2d")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(SEQUENCE_NAMES), default="conv2d")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -15,6 +15,10 @@
 //     128 B store to O[n][f][h][w0..w0+31].
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "../host/error.hpp"
 #include "common.cuh"
 #include "launch.h"
@@ -87,7 +91,15 @@ template <typename T, int FN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW,
               float* __restrict__ O, int F, int C, int R, int S, int OH, int OW, int tiles_h, int tiles_w,
-              int total_tiles) {
+              int total_tiles, long long* __restrict__ trace, int xflags) {
+#define CONV_TRACE(slot, v) \
+  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
+  auto gtimer = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return static_cast<long long>(t);
+  };
+  if (threadIdx.x == 0) CONV_TRACE(62, gtimer());
   constexpr int CK = 128 / sizeof(T);  // channels per 128 B row
   constexpr uint32_t W_CHUNK = FN * 128;
   constexpr uint32_t IDESC = instr_desc(ConvTraits<T>::kFormat, 128, FN, 0, 0);
@@ -139,7 +151,9 @@ __global__ void __launch_bounds__(192, 1)
         for (int ck = 0; ck < nck; ++ck)
           tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
       int it = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      long long pw = 0;
+      int pt = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++pt) {
         const int n = t / tiles_img;
         const int th = (t % tiles_img) / tiles_w;
         const int tw = t % tiles_w;
@@ -147,28 +161,42 @@ __global__ void __launch_bounds__(192, 1)
           for (int ck = 0; ck < nck; ++ck, ++it) {
             const int st = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
+            const long long w0 = trace ? clock64() : 0;
             mbar_wait(&empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&full[st], a_bytes);
-            tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * CK, tw * kBW + s, th * kBH, n);
+            if (trace) pw += clock64() - w0;
+            if (xflags & 4) {
+              mbar_arrive(&full[st]);
+            } else {
+              mbar_arrive_expect_tx(&full[st], a_bytes);
+              tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * CK, tw * kBW + s, th * kBH, n);
+            }
           }
+        CONV_TRACE(20 + pt, clock64());
       }
+      CONV_TRACE(61, pw);
     }
   } else if (warp == 1) {
     if (elect_one()) {
+      CONV_TRACE(0, clock64());
       mbar_wait(wbar, 0);
+      CONV_TRACE(1, clock64());
+      long long fw = 0;
       const uint32_t w_addr = smem_u32(wsm);
       const uint32_t a_base = smem_u32(asm_);
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
+        CONV_TRACE(2 + 2 * local, clock64());
         tc_fence_after();
         const uint32_t d = tmem + acc * FN;
         bool first = true;
         for (int s = 0; s < S; ++s)
           for (int ck = 0; ck < nck; ++ck, ++it) {
             const int st = it % STAGES;
+            const long long w0 = trace ? clock64() : 0;
             mbar_wait(&full[st], (it / STAGES) & 1);
+            if (trace) fw += clock64() - w0;
             tc_fence_after();
             const uint32_t a_addr = a_base + st * a_bytes;
             for (int r = 0; r < R; ++r) {
@@ -177,7 +205,8 @@ __global__ void __launch_bounds__(192, 1)
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = smem_desc_sw128(a_addr + r * (kBW * 128) + k * 32, 16, 1024);
                 const uint64_t bd = smem_desc_sw128(wa + k * 32, 16, 1024);
-                if constexpr (ConvTraits<T>::kF16)
+                if (xflags & 2) {
+                } else if constexpr (ConvTraits<T>::kF16)
                   mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
                 else
                   mma_tf32(d, ad, bd, IDESC, first ? 0u : 1u);
@@ -187,7 +216,9 @@ __global__ void __launch_bounds__(192, 1)
             mma_commit(&empty[st]);
           }
         mma_commit(&acc_full[acc]);
+        CONV_TRACE(3 + 2 * local, clock64());
       }
+      CONV_TRACE(60, fw);
     }
   } else {
     const int q = warp & 3;  // lane quarter = output row offset within the tile
@@ -207,7 +238,7 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[16];
         tmem_ld16(tmem + acc * FN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (ok) {
+        if (ok && !(xflags & 1)) {
 #pragma unroll
           for (int v = 0; v < 16; ++v)
             if (c + v < F) obase[(c + v) * fstride] = __uint_as_float(r[v]);
@@ -216,6 +247,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (warp == 2 && lane == 0) CONV_TRACE(40 + local, clock64());
     }
   }
   tc_fence_before();
@@ -224,6 +256,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);
   }
+  if (threadIdx.x == 0) CONV_TRACE(63, gtimer());
 }
 
 template <typename T, int FN>
@@ -274,7 +307,23 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_tc smem attribute");
     const int grid = std::min(total, a.sms);
-    kern<<<grid, 192, smem, st>>>(a.mapX, a.mapW, O, a.F, a.C, a.R, a.S, a.OH, a.OW, tiles_h, tiles_w, total);
+    static long long* trace = nullptr;  // developer knob: GENSOR_CONV_TRACE=<file> dumps clock64 marks
+    static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
+    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 148 * 64 * sizeof(long long) * 2), "trace");
+    if (trace) check_cuda(cudaMemsetAsync(trace, 0, 148 * 64 * sizeof(long long) * 2, st), "trace");
+    static const int xflags = std::getenv("GENSOR_CONV_XFLAGS") ? std::atoi(std::getenv("GENSOR_CONV_XFLAGS")) : 0;
+    kern<<<grid, 192, smem, st>>>(a.mapX, a.mapW, O, a.F, a.C, a.R, a.S, a.OH, a.OW, tiles_h, tiles_w, total, trace,
+                                  xflags);
+    if (trace) {
+      std::vector<long long> h(static_cast<size_t>(grid) * 64);
+      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
+      if (FILE* f = std::fopen(trace_path, "w")) {
+        for (int b = 0; b < grid; ++b) {
+          for (int i = 0; i < 64; ++i) std::fprintf(f, "%lld%c", h[static_cast<size_t>(b) * 64 + i], i == 63 ? '\n' : ' ');
+        }
+        std::fclose(f);
+      }
+    }
     check_cuda(cudaGetLastError(), "conv_tc launch");
     mk.mark(st);
     count_launch();

@@ -132,7 +132,8 @@ StreamArgs lower_stream(const OpDesc& op, const Sched& s, int sms) {
       a.wpr = 1;
       while (a.wpr < 8 && a.N / 4 >= static_cast<int64_t>(a.wpr) * 2 * 32 * 8) a.wpr *= 2;
     }
-    const int64_t step = op.kind == Kind::Gemv ? 8 / a.wpr : 1;
+    // rows a CTA covers per step: gemv 8/wpr, short-row softmax (warp per row, N <= 1024) 8
+    const int64_t step = op.kind == Kind::Gemv ? 8 / a.wpr : (a.N % 4 == 0 && a.N <= 1024 ? 8 : 1);
     // rows per unit: the level-1 m tile, halved while the grid would see fewer than 4 units per
     // resident CTA slot (8 x 256-thread CTAs per SM), so the persistent CTAs finish together
     int64_t rpu = std::max<int64_t>(step, t1(0));
@@ -275,9 +276,17 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           g.batch = static_cast<int>(op.batch);
           g.bf16 = bf16;
           // N tile from the schedule's level-1 n tile (UMMA N in [64, 256]); M tile = UMMA M 128
-          g.BN = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, 256));
-          pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"grid\":["
-             << (g.N + g.BN - 1) / g.BN << "," << (g.M + 127) / 128 << "," << g.batch << "],\"block\":192}";
+          // N tile: the schedule's level-1 n tile, clamped to the UMMA range [64, 256] (fp32 output:
+          // [64, 128], the epilogue staging must fit next to the pipeline); halved while the grid
+          // would leave SMs idle (fewer tiles than SMs).
+          const int bn_max = bf16 ? 256 : 128;
+          int bn = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, bn_max));
+          auto tiles = [&](int b) { return static_cast<int64_t>((g.M + 127) / 128) * ((g.N + b - 1) / b) * g.batch; };
+          while (bn > 64 && tiles(bn) < sms) bn /= 2;
+          g.BN = bn;
+          g.sms = sms;
+          pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
+             << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
           k->family = Family::ConvTc;
           k->launches = 3;

@@ -33,44 +33,56 @@ struct TcTraits<__nv_bfloat16> {
   static constexpr bool kF16Kind = true;
 };
 
+// Persistent: CTA b walks tiles b, b + grid, ... (n fastest, so consecutive CTAs share A rows in
+// L2). The smem ring continues across tiles; two TMEM accumulators let the epilogue of tile i
+// overlap the MMAs of tile i+1. Epilogue: tcgen05.ld 32 columns -> registers -> the warp's
+// 32-row staging slice in the 128 B-swizzled layout a TMA store expects -> one TMA store per
+// 128 B column block (full-line writes; OOB rows/columns clipped by the tensor map).
 template <typename T, typename TOut, int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TOut* __restrict__ C,
-              int M, int N, int K) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total) {
   constexpr int BM = 128;
   constexpr int BK = 128 / sizeof(T);           // K elements per 128 B swizzle row
   constexpr uint32_t A_BYTES = BM * 128;
   constexpr uint32_t B_BYTES = BN * 128;        // BN x BK elements
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   constexpr int B_CHUNKS = BN * sizeof(T) / 128;  // 128 B wide N chunks of the MN-major B tile
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;
   constexpr uint32_t IDESC = instr_desc(TcTraits<T>::kFormat, BM, BN, 0, 1);
+  constexpr int OUT_BLOCKS = BN * sizeof(TOut) / 128;  // 128 B column blocks of one output row
+  constexpr uint32_t STG_WARP = 32 * BN * sizeof(TOut);  // one epilogue warp's 32-row slice
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint8_t* staging = smem + STAGES * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * STG_WARP);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
-  const int b = blockIdx.z;
   const int nk = (K + BK - 1) / BK;
+  const int per_batch = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);  // one arrival per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapA);
     tma_prefetch(&mapB);
+    tma_prefetch(&mapC);
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -80,83 +92,108 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], STAGE);
-        uint8_t* a_s = smem + s * STAGE;
-        uint8_t* b_s = a_s + A_BYTES;
-        tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
+        const int m0 = mt * BM, n0 = nt * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE);
+          uint8_t* a_s = smem + s * STAGE;
+          uint8_t* b_s = a_s + A_BYTES;
+          tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
 #pragma unroll
-        for (int j = 0; j < B_CHUNKS; ++j)
-          tma_load_3d(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
+          for (int j = 0; j < B_CHUNKS; ++j)
+            tma_load_3d(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
+        }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(smem + s * STAGE);
-        const uint32_t b_addr = a_addr + A_BYTES;
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * STAGE);
+          const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 4 MMAs x 32 B of K (tf32 K=8, bf16 K=16)
-          const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-          // MN-major B: bf16 -> SW128 (8-row K groups, SBO 1024); tf32 -> SW128_BASE32B (4-row, SBO 512)
-          const uint64_t bd = TcTraits<T>::kF16Kind
-                                  ? smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 1024, 2)
-                                  : smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 512, 1);
-          if constexpr (TcTraits<T>::kF16Kind)
-            mma_f16(tmem, ad, bd, IDESC, (kb | k) != 0);
-          else
-            mma_tf32(tmem, ad, bd, IDESC, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // 4 MMAs x 32 B of K (tf32 K=8, bf16 K=16)
+            const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            // MN-major B: bf16 -> SW128 (8-row K groups, SBO 1024); tf32 -> SW128_BASE32B (4-row, SBO 512)
+            const uint64_t bd = TcTraits<T>::kF16Kind
+                                    ? smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 1024, 2)
+                                    : smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 512, 1);
+            if constexpr (TcTraits<T>::kF16Kind)
+              mma_f16(d, ad, bd, IDESC, (kb | k) != 0);
+            else
+              mma_tf32(d, ad, bd, IDESC, (kb | k) != 0);
+          }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&acc_full[acc]);
       }
-      mma_commit(tmem_full);
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    TOut* crow = C + (static_cast<int64_t>(b) * M + row) * N;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access = its 32 tile rows
+    uint8_t* stg = staging + q * STG_WARP;
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
+      const int m0 = mt * BM, n0 = nt * BN;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) bulk_wait_read<0>();  // the previous tile's TMA stores have read the slice
+      __syncwarp();
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, r);
-      tmem_ld_wait();
-      const int n = n0 + c;
-      if (row >= M || n >= N) continue;
-      if constexpr (sizeof(TOut) == 4) {
-        if (n + 16 <= N && (N & 3) == 0) {
-          float4* dst = reinterpret_cast<float4*>(crow + n);
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+        tmem_ld_wait();
+        if constexpr (sizeof(TOut) == 4) {  // 32 fp32 = one 128 B block, 8 chunks
+          uint8_t* blk = stg + (c / 32) * (32 * 128) + lane * 128;
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]),
-                                 __uint_as_float(r[4 * v + 3]));
-        } else {
-          for (int v = 0; v < 16 && n + v < N; ++v) crow[n + v] = __uint_as_float(r[v]);
-        }
-      } else {
-        if (n + 16 <= N && (N & 7) == 0) {
-          uint32_t p[8];
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(blk + ((k ^ (lane & 7)) << 4)) =
+                make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        } else {  // 32 bf16 = half a 128 B block, 4 chunks
+          uint8_t* blk = stg + (c / 64) * (32 * 128) + lane * 128;
+          const int k0 = (c % 64) / 8;
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1]));
-            p[v] = *reinterpret_cast<uint32_t*>(&h);
+          for (int k = 0; k < 4; ++k) {
+            uint32_t p[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * k + 2 * v]), __uint_as_float(r[8 * k + 2 * v + 1]));
+              p[v] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            *reinterpret_cast<uint4*>(blk + (((k0 + k) ^ (lane & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
           }
-          uint4* dst = reinterpret_cast<uint4*>(crow + n);
-          dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-          dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
-        } else {
-          for (int v = 0; v < 16 && n + v < N; ++v) crow[n + v] = __float2bfloat16_rn(__uint_as_float(r[v]));
         }
       }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&acc_empty[acc]);  // TMEM drained into registers/smem
+        if (m0 + q * 32 < M) {
+#pragma unroll
+          for (int j = 0; j < OUT_BLOCKS; ++j)
+            if (n0 + j * (128 / (int)sizeof(TOut)) < N)
+              tma_store_3d(&mapC, stg + j * (32 * 128), n0 + j * (128 / (int)sizeof(TOut)), m0 + q * 32, b);
+        }
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -180,32 +217,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <typename T, typename TOut, int BN, int STAGES>
 void run(const GemmTcArgs& a, cudaStream_t st) {
-  constexpr int BK = 128 / sizeof(T);
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
-  const size_t smem = STAGES * STAGE + 1024 + 256;
+  const size_t smem = STAGES * STAGE + 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
   auto kern = k_gemm_tc<T, TOut, BN, STAGES>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
              "gemm_tc smem attribute");
-  dim3 grid((a.N + BN - 1) / BN, (a.M + 127) / 128, a.batch);
-  kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, static_cast<TOut*>(a.C), a.M, a.N, a.K);
+  const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + BN - 1) / BN;
+  const int total = tiles_m * tiles_n * a.batch;
+  const int grid = std::min(total, a.sms);
+  kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total);
   check_cuda(cudaGetLastError(), "gemm_tc launch");
   count_launch();
-  (void)BK;
 }
 
+// Pipeline depth: as many stages as fit next to the epilogue staging (227 KB opt-in).
 template <typename T, typename TOut, int BN>
 void run_bn(const GemmTcArgs& a, cudaStream_t st) {
-  constexpr uint32_t STAGE = 128 * 128 + BN * 128;
-  constexpr int MAXS = static_cast<int>((200 * 1024) / STAGE);
+  constexpr size_t STAGE = 128 * 128 + BN * 128;
+  constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
+  constexpr int MAXS = static_cast<int>((227 * 1024 - 2048 - STG) / STAGE);
+  static_assert(MAXS >= 2, "gemm_tc tile does not fit shared memory");
   const int nk = (a.K + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T));
-  if (nk <= 1)
-    run<T, TOut, BN, 1>(a, st);
-  else if (nk <= 2 || MAXS < 4)
-    run<T, TOut, BN, 2>(a, st);
-  else if (MAXS < 6)
-    run<T, TOut, BN, 4>(a, st);
-  else
+  if (MAXS >= 6 && nk > 4)
     run<T, TOut, BN, 6>(a, st);
+  else if (MAXS >= 4)
+    run<T, TOut, BN, 4>(a, st);
+  else if (MAXS >= 3)
+    run<T, TOut, BN, 3>(a, st);
+  else
+    run<T, TOut, BN, 2>(a, st);
 }
 
 }  // namespace
@@ -242,7 +282,13 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
     a.last_A = A;
     a.last_B = B;
   }
-  a.C = C;
+  if (C != a.C) {  // output map: 128 B column blocks x 32 rows (one epilogue warp's slice)
+    const uint64_t dc[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.batch)};
+    const uint64_t sc[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.M * es};
+    const uint32_t bc[3] = {static_cast<uint32_t>(128 / es), 32, 1};
+    encode_map(&a.mapC, a.bf16, false, C, 3, dc, sc, bc);
+    a.C = C;
+  }
   if (a.bf16) {
     switch (a.BN) {
       case 64: run_bn<__nv_bfloat16, __nv_bfloat16, 64>(a, st); break;
@@ -252,8 +298,7 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
   } else {
     switch (a.BN) {
       case 64: run_bn<float, float, 64>(a, st); break;
-      case 128: run_bn<float, float, 128>(a, st); break;
-      default: run_bn<float, float, 256>(a, st); break;
+      default: run_bn<float, float, 128>(a, st); break;
     }
   }
 }

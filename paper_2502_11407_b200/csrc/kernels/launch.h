@@ -30,11 +30,12 @@ void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int ran
 
 // ---- tensor-core GEMM family (gemm_tc.cu) ----
 struct GemmTcArgs {
-  CUtensorMap mapA, mapB;  // rebuilt when the operand pointers change
+  CUtensorMap mapA, mapB, mapC;  // rebuilt when the operand / output pointers change
   const void* last_A = nullptr;
   const void* last_B = nullptr;
   void* C = nullptr;
   int M = 0, N = 0, K = 0, batch = 1, BN = 128;
+  int sms = 148;
   bool bf16 = false;
 };
 bool gemm_tc_supported(int M, int N, int K, int elem_bytes);

@@ -330,6 +330,52 @@ __global__ void __launch_bounds__(kSoftmaxThreads) k_softmax_reg(const float* __
   }
 }
 
+// Short rows (N <= 32 * 4 * VPL): one warp per row, the row in registers, warp-shuffle max and
+// fp64 sum — no shared memory, no block barriers (GPT-2 attention rows, N = 512).
+template <int VPL>
+__global__ void __launch_bounds__(kSoftmaxThreads) k_softmax_warp(const float* __restrict__ X, float* __restrict__ Y,
+                                                                  int64_t M, int64_t N, int64_t rows_per_unit,
+                                                                  int64_t units) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nv = N >> 2;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t r_end = min(M, (u + 1) * rows_per_unit);
+    for (int64_t m = u * rows_per_unit + warp; m < r_end; m += kSoftmaxThreads / 32) {
+      const float* row = X + m * N;
+      float4 v[VPL];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int64_t i = lane + 32 * q;
+        if (i < nv) {
+          v[q] = ld_stream4(row + 4 * i);
+          mx = fmaxf(mx, fmaxf(fmaxf(v[q].x, v[q].y), fmaxf(v[q].z, v[q].w)));
+        }
+      }
+      mx = warp_max(mx);
+      float ts = 0.0f;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int64_t i = lane + 32 * q;
+        if (i < nv) {
+          v[q].x = exp_shift(v[q].x, mx);
+          v[q].y = exp_shift(v[q].y, mx);
+          v[q].z = exp_shift(v[q].z, mx);
+          v[q].w = exp_shift(v[q].w, mx);
+          ts += (v[q].x + v[q].y) + (v[q].z + v[q].w);
+        }
+      }
+      const float inv = static_cast<float>(1.0 / warp_sum(static_cast<double>(ts)));
+      float* out = Y + m * N;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int64_t i = lane + 32 * q;
+        if (i < nv) st_stream4(out + 4 * i, make_float4(v[q].x * inv, v[q].y * inv, v[q].z * inv, v[q].w * inv));
+      }
+    }
+  }
+}
+
 // Any N (unaligned or longer than the register budget): max pass, sum pass, write pass.
 __global__ void __launch_bounds__(kSoftmaxThreads) k_softmax_any(const float* __restrict__ X, float* __restrict__ Y,
                                                                  int64_t M, int64_t N, int64_t rows_per_unit,
@@ -720,7 +766,10 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
                                                                       static_cast<float*>(out), a.M, a.N,
                                                                       a.rows_per_unit, units);
       };
-      if (vec && nv <= kSoftmaxThreads * 1) go(k_softmax_reg<1>);
+      if (vec && nv <= 32 * 2) go(k_softmax_warp<2>);
+      else if (vec && nv <= 32 * 4) go(k_softmax_warp<4>);
+      else if (vec && nv <= 32 * 8) go(k_softmax_warp<8>);
+      else if (vec && nv <= kSoftmaxThreads * 1) go(k_softmax_reg<1>);
       else if (vec && nv <= kSoftmaxThreads * 2) go(k_softmax_reg<2>);
       else if (vec && nv <= kSoftmaxThreads * 4) go(k_softmax_reg<4>);
       else if (vec && nv <= kSoftmaxThreads * 8) go(k_softmax_reg<8>);
