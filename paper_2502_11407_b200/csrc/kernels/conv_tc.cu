@@ -1,18 +1,22 @@
 // Tensor-core implicit-GEMM conv2d (stride 1), instantiated from a constructed conv2d schedule:
 //   O[n][f][h][w] = sum_{c,r,s} I[n][c][h+r][w+s] * K[f][c][r][s]   (op_spec.cpp:177-181)
-// GEMM view: M = output positions (h, w), N = f, K = (r, s, c).
+// GEMM view: M = output positions, N = f, K = (r, s, c). ONE launch, reference layouts in and out:
 //
-// Step 1 (pre-pass, HBM-bound): NCHW input -> NHWC X (so c is the contiguous K dim a TMA box
-// can load as 128 B swizzled rows) and K[f][c][r][s] -> W'[r][s][f][c].
-// Step 2 (persistent tcgen05 kernel, one CTA per SM):
-//   * the whole W' lives in shared memory for the CTA's lifetime (loaded once by TMA);
-//   * an output tile is BH=4 rows x BW=32 columns of one image (M = 128 = one UMMA M);
-//   * for each (s, 128 B c-chunk) the producer loads ONE box of (BH+R-1) x BW positions; the R
-//     row shifts are 1024 B-aligned sub-views of that box, so each A row is fetched once per s
-//     instead of once per (r, s) — a 3x cut of the L2->SM operand traffic for 3x3 filters;
-//   * TMEM holds two 128 x FN fp32 accumulators so the epilogue of tile i overlaps tile i+1;
-//   * epilogue warp q owns output row h0+q: lane = w, each tcgen05.ld column f is one coalesced
-//     128 B store to O[n][f][h][w0..w0+31].
+//   * output tile = 8 rows x 2 images x 8 columns = 128 positions (one UMMA M), laid out in shared
+//     memory as row rho = h*16 + img*8 + w. A shift by filter row r is then rho + 16r (2 KB, a
+//     whole number of 1 KB swizzle atoms), so ONE staged box of (8+R-1) x 2 x 8 positions per
+//     (s, 128 B channel chunk) serves all R row shifts (3x fewer staged bytes for 3x3). The tile
+//     divides 56 x 56 exactly: C = [16,64,58,58] is 392 tiles, no idle lanes;
+//   * the A boxes are built by 8 producer warps straight from the NCHW input (software im2col:
+//     coalesced 32 B row runs, 16 B swizzled shared stores, fence.proxy.async) — no NHWC pre-pass
+//     and no extra HBM round trip;
+//   * the filter bank is converted to the K-major layout W'[r][s][f][c] by every CTA straight into
+//     shared memory at start (coalesced 16 B loads of K[f][c][r][s]), where it stays for the CTA's
+//     lifetime; each input row run is loaded once per channel chunk and shifted across lanes
+//     (shuffles) for the S filter columns;
+//   * one thread issues tcgen05.mma (kind::tf32 or kind::f16) into two TMEM accumulators
+//     (double-buffered: the epilogue of tile i overlaps the MMAs of tile i+1);
+//   * 4 epilogue warps: tcgen05.ld -> streaming stores into NCHW.
 #include <cuda_bf16.h>
 
 #include <cstdio>
@@ -30,183 +34,216 @@ namespace {
 
 using namespace tc;
 
-constexpr int kBH = 4;
-constexpr int kBW = 32;
-
-// NCHW fp32 -> NHWC (fp32 or bf16), 32x32 tiles of [c][w] per (n, h) through shared memory.
-template <typename TX>
-__global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ in, TX* __restrict__ out, int C, int H,
-                                                      int W) {
-  __shared__ float tile[32][33];
-  const int nh = blockIdx.z;  // n * H + h
-  const int c0 = blockIdx.y * 32, w0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t n = nh / H, h = nh % H;
-  const float* src = in + (n * C) * static_cast<int64_t>(H) * W + h * W;
-#pragma unroll
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i, w = w0 + tx;
-    tile[i][tx] = (c < C && w < W) ? src[static_cast<int64_t>(c) * H * W + w] : 0.0f;
-  }
-  __syncthreads();
-  TX* dst = out + (static_cast<int64_t>(nh) * W) * C;
-#pragma unroll
-  for (int i = ty; i < 32; i += 8) {
-    const int w = w0 + i, c = c0 + tx;
-    if (w < W && c < C) dst[static_cast<int64_t>(w) * C + c] = from_f32<TX>(tile[tx][i]);
-  }
-}
-
-template <typename TX>
-__global__ void k_weights_rsfc(const float* __restrict__ k, TX* __restrict__ out, int F, int C, int R, int S) {
-  const int64_t total = static_cast<int64_t>(F) * C * R * S;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // out index (r, s, f, c)
-    int64_t t = i;
-    const int c = t % C;
-    t /= C;
-    const int f = t % F;
-    t /= F;
-    const int s = t % S;
-    const int r = static_cast<int>(t / S);
-    out[i] = from_f32<TX>(k[((static_cast<int64_t>(f) * C + c) * R + r) * S + s]);
-  }
-}
+constexpr int kTH = 8;       // output rows per tile
+constexpr int kTI = 2;       // images per tile
+constexpr int kTW = 8;       // output columns per tile
+constexpr int kProducerWarps = 8;  // two groups of 4 warps, each group fills every other stage
+constexpr int kGroupThreads = 128;
+constexpr int kThreads = 32 * (kProducerWarps + 1 + 4);  // producers, MMA, 4 epilogue warps
 
 template <typename T>
 struct ConvTraits;
 template <>
 struct ConvTraits<float> {
-  static constexpr uint32_t kFormat = 2;
+  static constexpr uint32_t kFormat = 2;  // tf32
   static constexpr bool kF16 = false;
 };
 template <>
 struct ConvTraits<__nv_bfloat16> {
-  static constexpr uint32_t kFormat = 1;
+  static constexpr uint32_t kFormat = 1;  // bf16
   static constexpr bool kF16 = true;
 };
 
+__device__ __forceinline__ uint4 pack16(const float (&v)[4]) {
+  return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+}
+__device__ __forceinline__ uint4 pack16(const float (&v)[8]) {
+  uint32_t p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    p[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
 template <typename T, int FN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
-    k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW,
-              float* __restrict__ O, int F, int C, int R, int S, int OH, int OW, int tiles_h, int tiles_w,
-              int total_tiles, long long* __restrict__ trace, int xflags) {
+__global__ void __launch_bounds__(kThreads, 1)
+    k_conv_tc(const float* __restrict__ I, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
+              int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
+              long long* __restrict__ trace) {
+  // developer trace (GENSOR_CONV_TRACE=<file>): clock64 marks per CTA, 64 slots
 #define CONV_TRACE(slot, v) \
   if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
-  auto gtimer = []() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return static_cast<long long>(t);
-  };
-  if (threadIdx.x == 0) CONV_TRACE(62, gtimer());
-  constexpr int CK = 128 / sizeof(T);  // channels per 128 B row
-  constexpr uint32_t W_CHUNK = FN * 128;
+  constexpr int CK = 128 / sizeof(T);        // channels per 128 B row
+  constexpr int QV = 16 / sizeof(T);         // channels per 16 B chunk
+  constexpr uint32_t W_CHUNK = FN * 128;     // one (r, s, c-chunk) slice of W'
   constexpr uint32_t IDESC = instr_desc(ConvTraits<T>::kFormat, 128, FN, 0, 0);
   constexpr uint32_t TMEM_COLS = 2 * FN;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nck = (C + CK - 1) / CK;
+  const int box_rows = (kTH + R - 1) * kTI * kTW;  // staged positions per (s, c-chunk)
   const uint32_t w_bytes = static_cast<uint32_t>(R * S * nck) * W_CHUNK;
-  const uint32_t a_bytes = static_cast<uint32_t>((kBH + R - 1) * kBW * 128);
+  const uint32_t a_bytes = static_cast<uint32_t>(box_rows * 128);
   uint8_t* wsm = smem;
-  uint8_t* asm_ = smem + w_bytes;  // STAGES x a_bytes (each a multiple of 1024)
+  uint8_t* asm_ = smem + w_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + STAGES * a_bytes);
   uint64_t* empty = full + STAGES;
   uint64_t* wbar = empty + STAGES;
-  uint64_t* acc_full = wbar + 1;   // [2]
+  uint64_t* acc_full = wbar + 1;       // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tiles_img = tiles_h * tiles_w;
+  constexpr int kMmaWarp = kProducerWarps;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kGroupThreads);
       mbar_init(&empty[s], 1);
     }
     mbar_init(wbar, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);  // one arrival per epilogue warp
+      mbar_init(&acc_empty[i], 4);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch(&mapX);
-      tma_prefetch(&mapW);
-      // resident weights: one (F x 128 B) K-major chunk per (r, s, c-chunk)
-      mbar_arrive_expect_tx(wbar, w_bytes);
-      for (int rs = 0; rs < R * S; ++rs)
-        for (int ck = 0; ck < nck; ++ck)
-          tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
-      int it = 0;
-      long long pw = 0;
-      int pt = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++pt) {
-        const int n = t / tiles_img;
-        const int th = (t % tiles_img) / tiles_w;
-        const int tw = t % tiles_w;
-        for (int s = 0; s < S; ++s)
-          for (int ck = 0; ck < nck; ++ck, ++it) {
-            const int st = it % STAGES;
-            const uint32_t ph = (it / STAGES) & 1;
-            const long long w0 = trace ? clock64() : 0;
-            mbar_wait(&empty[st], ph ^ 1);
-            if (trace) pw += clock64() - w0;
-            if (xflags & 4) {
-              mbar_arrive(&full[st]);
-            } else {
-              mbar_arrive_expect_tx(&full[st], a_bytes);
-              tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * CK, tw * kBW + s, th * kBH, n);
+  if (warp < kProducerWarps) {
+    // ---- software im2col producers: A box rows rho = hh*16 + img*8 + w, 128 B of channels ----
+    // One PASS = the S stages (s = 0..S-1) of one 128 B channel chunk: each input row run
+    // (8 + S - 1 columns) is loaded ONCE and shifted across lanes with shuffles for every s.
+    // Group g (warps 4g..4g+3) takes passes p = g (mod 2); lanes = (column wl, 16 B chunk cq).
+    const int grp = warp >> 2, pw = warp & 3;
+    const int wl = lane & 7, cq = lane >> 3;
+    const int64_t plane = static_cast<int64_t>(H) * W;
+    const int items = (kTH + R - 1) * kTI * 2;  // (hh, img, half) rows per pass
+    // tf32: a warp's whole share of a pass (<= kB items) is loaded before any store, so each of
+    // the S stages is published as soon as it is written; bf16 (twice the channels per 16 B
+    // chunk) works in two register batches and publishes the S stages at the end of the pass.
+    constexpr int kB = sizeof(T) == 4 ? 10 : 5;
+    int it = 0, pass = 0, pstage = 0;
+    long long pwait = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int np = t / tiles_img;
+      const int h0 = ((t % tiles_img) / tiles_w) * kTH;
+      const int w0 = (t % tiles_w) * kTW;
+      for (int ck = 0; ck < nck; ++ck, ++pass, it += S) {
+        if ((pass & 1) != grp) continue;
+        const bool one_batch = items <= 4 * kB;
+        for (int base = pw; base < items; base += 4 * kB) {
+          float v0[kB][QV], v8[kB][QV];
+#pragma unroll
+          for (int b = 0; b < kB; ++b) {
+            const int item = base + 4 * b;
+            const int half = item & 1, img = (item >> 1) & 1, hh = item >> 2;
+            const int n = np * kTI + img, hi = h0 + hh;
+            const int c0 = ck * CK + (half * 4 + cq) * QV;
+            const bool row_ok = item < items && n < N && hi < H;
+            const int wa = w0 + wl, wb = w0 + wl + 8;
+            const float* src = I + ((static_cast<int64_t>(n) * C + c0) * H + hi) * static_cast<int64_t>(W);
+#pragma unroll
+            for (int j = 0; j < QV; ++j) {
+              const bool cj = row_ok && c0 + j < C;
+              v0[b][j] = (cj && wa < W) ? __ldg(src + j * plane + wa) : 0.0f;
+              v8[b][j] = (cj && wl < S - 1 && wb < W) ? __ldg(src + j * plane + wb) : 0.0f;
             }
           }
-        CONV_TRACE(20 + pt, clock64());
+          for (int s = 0; s < S; ++s) {
+            const int k = it + s;
+            if (base == pw) {  // first batch: the slot must have been consumed by the MMA
+              const long long tw0 = trace ? clock64() : 0;
+              mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
+              if (trace) pwait += clock64() - tw0;
+            }
+            uint8_t* box = asm_ + (k % STAGES) * a_bytes;
+            const int src_lane = (lane & ~7) | ((wl + s) & 7);
+            const bool lo = wl + s < 8;
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+              float v[QV];
+              if (s == 0) {
+#pragma unroll
+                for (int j = 0; j < QV; ++j) v[j] = v0[b][j];
+              } else {
+#pragma unroll
+                for (int j = 0; j < QV; ++j) {
+                  const float x0 = __shfl_sync(0xffffffffu, v0[b][j], src_lane);
+                  const float x8 = __shfl_sync(0xffffffffu, v8[b][j], src_lane);
+                  v[j] = lo ? x0 : x8;
+                }
+              }
+              const int item = base + 4 * b;
+              if (item < items) {
+                const int half = item & 1, img = (item >> 1) & 1, hh = item >> 2;
+                const int q = half * 4 + cq;
+                const int rho = hh * (kTI * kTW) + img * kTW + wl;
+                *reinterpret_cast<uint4*>(box + rho * 128 + ((q ^ (rho & 7)) << 4)) = pack16(v);
+              }
+            }
+            if (one_batch) {  // stage s complete: publish it now
+              fence_proxy_async_smem();
+              mbar_arrive(&full[k % STAGES]);
+            }
+          }
+        }
+        if (!one_batch) {
+          fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+          for (int s = 0; s < S; ++s) mbar_arrive(&full[(it + s) % STAGES]);
+        }
+        if (warp == 0 && lane == 0 && pstage < 20) CONV_TRACE(20 + pstage, clock64());
+        ++pstage;
       }
-      CONV_TRACE(61, pw);
     }
-  } else if (warp == 1) {
+    if (warp == 0 && lane == 0) CONV_TRACE(61, pwait);
+  } else if (warp == kMmaWarp) {
     if (elect_one()) {
       CONV_TRACE(0, clock64());
+      // W' is written by the preceding conversion launch (programmatic dependent launch: this
+      // grid starts early and only this thread waits for the primary grid's results)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      tma_prefetch(&mapW);
+      mbar_arrive_expect_tx(wbar, w_bytes);
+      for (int rs = 0; rs < R * S; ++rs)
+        for (int ck = 0; ck < nck; ++ck) tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
       mbar_wait(wbar, 0);
-      CONV_TRACE(1, clock64());
-      long long fw = 0;
+      CONV_TRACE(2, clock64());
+      long long fwait = 0;
       const uint32_t w_addr = smem_u32(wsm);
       const uint32_t a_base = smem_u32(asm_);
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
-        CONV_TRACE(2 + 2 * local, clock64());
+        if (local < 4) CONV_TRACE(3 + 2 * local, clock64());
         tc_fence_after();
         const uint32_t d = tmem + acc * FN;
         bool first = true;
-        for (int s = 0; s < S; ++s)
-          for (int ck = 0; ck < nck; ++ck, ++it) {
+        for (int ck = 0; ck < nck; ++ck)
+          for (int s = 0; s < S; ++s, ++it) {
             const int st = it % STAGES;
-            const long long w0 = trace ? clock64() : 0;
+            const long long tw0 = trace ? clock64() : 0;
             mbar_wait(&full[st], (it / STAGES) & 1);
-            if (trace) fw += clock64() - w0;
+            if (trace) fwait += clock64() - tw0;
             tc_fence_after();
             const uint32_t a_addr = a_base + st * a_bytes;
             for (int r = 0; r < R; ++r) {
               const uint32_t wa = w_addr + ((r * S + s) * nck + ck) * W_CHUNK;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                const uint64_t ad = smem_desc_sw128(a_addr + r * (kBW * 128) + k * 32, 16, 1024);
+                const uint64_t ad = smem_desc_sw128(a_addr + r * (kTI * kTW * 128) + k * 32, 16, 1024);
                 const uint64_t bd = smem_desc_sw128(wa + k * 32, 16, 1024);
-                if (xflags & 2) {
-                } else if constexpr (ConvTraits<T>::kF16)
+                if constexpr (ConvTraits<T>::kF16)
                   mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
                 else
                   mma_tf32(d, ad, bd, IDESC, first ? 0u : 1u);
@@ -216,47 +253,66 @@ __global__ void __launch_bounds__(192, 1)
             mma_commit(&empty[st]);
           }
         mma_commit(&acc_full[acc]);
-        CONV_TRACE(3 + 2 * local, clock64());
+        if (local < 4) CONV_TRACE(4 + 2 * local, clock64());
       }
-      CONV_TRACE(60, fw);
+      CONV_TRACE(60, fwait);
     }
   } else {
-    const int q = warp & 3;  // lane quarter = output row offset within the tile
+    // ---- epilogue warps: drain TMEM into NCHW ----
+    const int q = warp & 3;  // TMEM lane quarter = tile rows m in [32q, 32q+32)
+    // position of TMEM lane m = 32q + lane: rho = hh*16 + img*8 + w
+    const int hh = (q * 32 + lane) / (kTI * kTW), img = (lane >> 3) & 1, wl = lane & 7;
+    const int64_t fstride = static_cast<int64_t>(OH) * OW;
     int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int n = t / tiles_img;
-      const int h = ((t % tiles_img) / tiles_w) * kBH + q;
-      const int w = (t % tiles_w) * kBW + lane;
+      const int n = (t / tiles_img) * kTI + img;
+      const int h = ((t % tiles_img) / tiles_w) * kTH + hh;
+      const int w = (t % tiles_w) * kTW + wl;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
-      const bool ok = h < OH && w < OW;
-      float* obase = O + ((static_cast<int64_t>(n) * F) * OH + h) * OW + w;
-      const int64_t fstride = static_cast<int64_t>(OH) * OW;
+      const bool ok = n < N && h < OH && w < OW;
+      float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
 #pragma unroll 1
-      for (int c = 0; c < FN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + acc * FN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+      for (int c = 0; c < FN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * FN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (ok && !(xflags & 1)) {
+        if (ok) {
 #pragma unroll
-          for (int v = 0; v < 16; ++v)
-            if (c + v < F) obase[(c + v) * fstride] = __uint_as_float(r[v]);
+          for (int v = 0; v < 32; ++v)
+            if (c + v < F) __stcs(obase + (c + v) * fstride, __uint_as_float(r[v]));
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      if (warp == 2 && lane == 0) CONV_TRACE(40 + local, clock64());
+      if (warp == kMmaWarp + 1 && lane == 0 && local < 4) CONV_TRACE(40 + local, clock64());
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);
   }
-  if (threadIdx.x == 0) CONV_TRACE(63, gtimer());
+}
+
+// K[f][c][r][s] -> W'[r][s][f][c] (K-major B operand rows for the TMA), the primary grid of the
+// programmatic dependent launch pair: it lets the conv grid launch at once.
+template <typename T>
+__global__ void __launch_bounds__(256) k_filters_kmajor(const float* __restrict__ K, T* __restrict__ Wt, int F, int C,
+                                                        int RS) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t total = static_cast<int64_t>(F) * C * RS;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // e indexes the source (coalesced reads): e = (f*C + c)*RS + rs
+    const int rs = static_cast<int>(e % RS);
+    const int64_t fc = e / RS;
+    const int c = static_cast<int>(fc % C), f = static_cast<int>(fc / C);
+    Wt[(static_cast<int64_t>(rs) * F + f) * C + c] = from_f32<T>(__ldg(K + e));
+  }
 }
 
 template <typename T, int FN>
@@ -264,63 +320,53 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
   constexpr int CK = 128 / sizeof(T);
   const int nck = (a.C + CK - 1) / CK;
   const size_t w_bytes = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
-  const size_t a_bytes = static_cast<size_t>((kBH + a.R - 1) * kBW * 128);
-  T* X = static_cast<T*>(a.ws_x);
-  T* Wt = static_cast<T*>(a.ws_w);
-  // pre-pass: layouts for TMA
-  mk.mark(st);
-  {
-    dim3 grid((a.W + 31) / 32, (a.C + 31) / 32, a.N * a.H);
-    k_nchw_to_nhwc<T><<<grid, 256, 0, st>>>(I, X, a.C, a.H, a.W);
-    check_cuda(cudaGetLastError(), "nchw_to_nhwc");
-    mk.mark(st);
-    const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
-    k_weights_rsfc<T><<<static_cast<unsigned>(std::min<int64_t>(1184, (wt + 255) / 256)), 256, 0, st>>>(
-        K, Wt, a.F, a.C, a.R, a.S);
-    check_cuda(cudaGetLastError(), "weights_rsfc");
-    mk.mark(st);
-    count_launch(2);
-  }
+  const size_t a_bytes = static_cast<size_t>((kTH + a.R - 1) * kTI * kTW * 128);
+  const int tiles_h = (a.OH + kTH - 1) / kTH, tiles_w = (a.OW + kTW - 1) / kTW;
+  const int total = ((a.N + kTI - 1) / kTI) * tiles_h * tiles_w;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  int stages = static_cast<int>((budget - w_bytes) / a_bytes);
+  if (stages > 6) stages = 6;
+  const int grid = std::min(total, a.sms);
   if (!a.maps_ready) {
     const int es = sizeof(T);
-    const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.H),
-                            static_cast<uint64_t>(a.N)};
-    const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.C) * a.W * es,
-                            static_cast<uint64_t>(a.C) * a.W * a.H * es};
-    const uint32_t bx[4] = {static_cast<uint32_t>(CK), static_cast<uint32_t>(kBW),
-                            static_cast<uint32_t>(kBH + a.R - 1), 1};
-    encode_map(&a.mapX, es == 2, es == 4, X, 4, dx, sx, bx);
     const uint64_t dw[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.F),
                             static_cast<uint64_t>(a.R) * a.S};
     const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.C) * a.F * es};
     const uint32_t bw[3] = {static_cast<uint32_t>(CK), static_cast<uint32_t>(FN), 1};
-    encode_map(&a.mapW, es == 2, es == 4, Wt, 3, dw, sw, bw);
+    encode_map(&a.mapW, es == 2, es == 4, a.ws_w, 3, dw, sw, bw);
     a.maps_ready = true;
   }
-  const int tiles_h = (a.OH + kBH - 1) / kBH, tiles_w = (a.OW + kBW - 1) / kBW;
-  const int total = a.N * tiles_h * tiles_w;
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  int stages = static_cast<int>((budget - w_bytes) / a_bytes);
-  if (stages >= 4) stages = 4;
   auto launch = [&](auto kern) {
     const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + 256;
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_tc smem attribute");
-    const int grid = std::min(total, a.sms);
-    static long long* trace = nullptr;  // developer knob: GENSOR_CONV_TRACE=<file> dumps clock64 marks
+    mk.mark(st);
+    const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
+    k_filters_kmajor<T><<<static_cast<unsigned>(std::min<int64_t>(a.sms, (wt + 255) / 256)), 256, 0, st>>>(
+        K, static_cast<T*>(a.ws_w), a.F, a.C, a.R * a.S);
+    check_cuda(cudaGetLastError(), "filters_kmajor launch");
+    count_launch();
     static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
-    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 148 * 64 * sizeof(long long) * 2), "trace");
-    if (trace) check_cuda(cudaMemsetAsync(trace, 0, 148 * 64 * sizeof(long long) * 2, st), "trace");
-    static const int xflags = std::getenv("GENSOR_CONV_XFLAGS") ? std::atoi(std::getenv("GENSOR_CONV_XFLAGS")) : 0;
-    kern<<<grid, 192, smem, st>>>(a.mapX, a.mapW, O, a.F, a.C, a.R, a.S, a.OH, a.OW, tiles_h, tiles_w, total, trace,
-                                  xflags);
-    if (trace) {
+    static long long* trace = nullptr;
+    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, I, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
+                                  tiles_w, total, trace),
+               "conv_tc launch");
+    if (trace) {  // developer path: synchronous dump of the last launch
       std::vector<long long> h(static_cast<size_t>(grid) * 64);
       check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
       if (FILE* f = std::fopen(trace_path, "w")) {
-        for (int b = 0; b < grid; ++b) {
-          for (int i = 0; i < 64; ++i) std::fprintf(f, "%lld%c", h[static_cast<size_t>(b) * 64 + i], i == 63 ? '\n' : ' ');
-        }
+        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
         std::fclose(f);
       }
     }
@@ -328,14 +374,16 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     mk.mark(st);
     count_launch();
   };
-  if (stages >= 4)
-    launch(k_conv_tc<T, FN, 4>);
-  else if (stages == 3)
-    launch(k_conv_tc<T, FN, 3>);
-  else if (stages == 2)
-    launch(k_conv_tc<T, FN, 2>);
-  else
-    throw Error(Code::Unsupported, "conv_tc: filter bank does not fit in shared memory");
+  switch (stages) {
+    case 1: launch(k_conv_tc<T, FN, 1>); break;
+    case 2: launch(k_conv_tc<T, FN, 2>); break;
+    case 3: launch(k_conv_tc<T, FN, 3>); break;
+    case 4: launch(k_conv_tc<T, FN, 4>); break;
+    case 5: launch(k_conv_tc<T, FN, 5>); break;
+    case 6: launch(k_conv_tc<T, FN, 6>); break;
+    default:
+      throw Error(Code::Unsupported, "conv_tc: filter bank does not fit in shared memory");
+  }
 }
 
 }  // namespace
@@ -345,17 +393,16 @@ size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16) {
   int FN = 32;
   while (FN < F) FN *= 2;
   const size_t nck = (C + CK - 1) / CK;
-  return static_cast<size_t>(R) * S * nck * FN * 128 + 2 * static_cast<size_t>((kBH + R - 1) * kBW * 128);
+  return static_cast<size_t>(R) * S * nck * FN * 128 + 2 * static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
 }
 
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
   const int es = bf16 ? 2 : 4;
-  return stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 &&
+  return stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8 &&
          conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256;
 }
 
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {
-  if (I != a.last_I || K != a.last_K) a.last_I = I, a.last_K = K;
   const float* i = static_cast<const float*>(I);
   const float* k = static_cast<const float*>(K);
   float* o = static_cast<float*>(O);

@@ -289,8 +289,8 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
              << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
           k->family = Family::ConvTc;
-          k->launches = 3;
-          k->launch_names = {"nchw_to_nhwc", "weights_rsfc", "conv_tc"};
+          k->launches = 1;
+          k->launch_names = {"conv_tc"};
           ConvTcArgs& c = k->conv;
           c.N = static_cast<int>(op.param("N"));
           c.C = static_cast<int>(op.param("C"));
@@ -303,15 +303,15 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.OW = static_cast<int>(op.param("OW"));
           c.bf16 = bf16;
           c.sms = sms;
-          const size_t es = bf16 ? 2 : 4;
-          const size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
-          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
-          check_cuda(cudaMalloc(&k->ws, xb + wb + 256), "conv workspace");
-          c.ws_x = k->ws;
-          c.ws_w = static_cast<char*>(k->ws) + ((xb + 255) & ~size_t(255));
-          const int tiles = c.N * ((c.OH + 3) / 4) * ((c.OW + 31) / 32);
-          pi << "{\"family\":\"conv_tc\",\"M_tile\":\"4x32 positions\",\"FN\":" << c.F << ",\"tiles\":" << tiles
-             << ",\"grid\":" << std::min(tiles, sms) << ",\"block\":192,\"prepass\":\"nchw->nhwc, kfcrs->rsfc\"}";
+          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * (bf16 ? 2 : 4);
+          check_cuda(cudaMalloc(&k->ws, wb), "conv workspace");
+          c.ws_w = k->ws;
+          k->launches = 2;  // filter conversion + conv (programmatic dependent launch), timed as one span
+          k->launch_names = {"conv_tc"};
+          const int tiles = ((c.N + 1) / 2) * ((c.OH + 7) / 8) * ((c.OW + 7) / 8);
+          pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F
+             << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
+             << ",\"block\":416,\"launches\":2,\"im2col\":\"in-kernel from NCHW\",\"filters\":\"K-major conversion launch + PDL\"}";
         } else {
           throw Error(Code::Unsupported, std::string(kVariantNames[k->variant]) + " not available for " + op.label());
         }

@@ -43,12 +43,9 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
 
 // ---- tensor-core implicit-GEMM conv2d family (conv_tc.cu) ----
 struct ConvTcArgs {
-  CUtensorMap mapX, mapW;  // over the workspace layouts, built once
+  CUtensorMap mapW;   // over the W'[r][s][f][c] workspace, built once
   bool maps_ready = false;
-  const void* last_I = nullptr;
-  const void* last_K = nullptr;
-  void* ws_x = nullptr;  // NHWC input copy
-  void* ws_w = nullptr;  // [R][S][F][C] filter copy
+  void* ws_w = nullptr;  // W' workspace, rewritten by the filter-conversion launch of every execute
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
   int sms = 148;
   bool bf16 = false;
