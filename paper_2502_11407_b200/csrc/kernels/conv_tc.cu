@@ -54,29 +54,20 @@ struct ConvTraits<__nv_bfloat16> {
   static constexpr bool kF16 = true;
 };
 
-__device__ __forceinline__ uint4 pack16(const float (&v)[4]) {
-  return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
-}
-__device__ __forceinline__ uint4 pack16(const float (&v)[8]) {
-  uint32_t p[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-    p[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  return make_uint4(p[0], p[1], p[2], p[3]);
+__device__ __forceinline__ void st_shared_v4(void* p, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
 }
 
 template <typename T, int FN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_conv_tc(const float* __restrict__ I, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
+    k_conv_tc(const T* __restrict__ X, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
               int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
               long long* __restrict__ trace) {
   // developer trace (GENSOR_CONV_TRACE=<file>): clock64 marks per CTA, 64 slots
 #define CONV_TRACE(slot, v) \
   if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int CK = 128 / sizeof(T);        // channels per 128 B row
-  constexpr int QV = 16 / sizeof(T);         // channels per 16 B chunk
   constexpr uint32_t W_CHUNK = FN * 128;     // one (r, s, c-chunk) slice of W'
   constexpr uint32_t IDESC = instr_desc(ConvTraits<T>::kFormat, 128, FN, 0, 0);
   constexpr uint32_t TMEM_COLS = 2 * FN;
@@ -120,18 +111,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kProducerWarps) {
-    // ---- software im2col producers: A box rows rho = hh*16 + img*8 + w, 128 B of channels ----
-    // One PASS = the S stages (s = 0..S-1) of one 128 B channel chunk: each input row run
-    // (8 + S - 1 columns) is loaded ONCE and shifted across lanes with shuffles for every s.
-    // Group g (warps 4g..4g+3) takes passes p = g (mod 2); lanes = (column wl, 16 B chunk cq).
+    // ---- producers: A box rows rho = hh*16 + img*8 + w (128 B of channels) from the NHWC copy.
+    // One PASS = the S stages (s = 0..S-1) of one 128 B channel chunk: each (hh, img, column)
+    // 16 B chunk of X is loaded ONCE (LDG.128, 8 lanes per 128 B position row) and stored into
+    // every s-stage whose tile column it feeds (column x feeds w = x - s).
+    // Group g (warps 4g..4g+3) takes passes p = g (mod 2).
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
     const int grp = warp >> 2, pw = warp & 3;
-    const int wl = lane & 7, cq = lane >> 3;
-    const int64_t plane = static_cast<int64_t>(H) * W;
-    const int items = (kTH + R - 1) * kTI * 2;  // (hh, img, half) rows per pass
-    // tf32: a warp's whole share of a pass (<= kB items) is loaded before any store, so each of
-    // the S stages is published as soon as it is written; bf16 (twice the channels per 16 B
-    // chunk) works in two register batches and publishes the S stages at the end of the pass.
-    constexpr int kB = sizeof(T) == 4 ? 10 : 5;
+    const int q = lane & 7, sub = lane >> 3;  // 16 B chunk within the 128 B row, row slot 0..3
+    const int cols = kTW + S - 1;              // input columns per tile row
+    const int rows = (kTH + R - 1) * kTI;      // (hh, img) rows per pass
+    const int nrow_items = rows * cols;        // position rows to move per pass
     int it = 0, pass = 0, pstage = 0;
     long long pwait = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -140,65 +130,82 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int w0 = (t % tiles_w) * kTW;
       for (int ck = 0; ck < nck; ++ck, ++pass, it += S) {
         if ((pass & 1) != grp) continue;
-        const bool one_batch = items <= 4 * kB;
-        for (int base = pw; base < items; base += 4 * kB) {
-          float v0[kB][QV], v8[kB][QV];
+        // 4 position rows per warp instruction (8 lanes x 16 B each); a group moves 16 per step
+        auto load_row = [&](int ri) -> uint4 {
+          const int x = ri % cols, rr = ri / cols;  // input column, (hh, img) row
+          const int img = rr & 1, hh = rr >> 1;
+          const int n = np * kTI + img, hi = h0 + hh, wi = w0 + x;
+          const bool ok = ri < nrow_items && n < N && hi < H && wi < W &&
+                          (ck * CK + q * static_cast<int>(16 / sizeof(T))) < C;
+          const uint4* src =
+              reinterpret_cast<const uint4*>(X + (((static_cast<int64_t>(n) * H + hi) * W + wi) * C + ck * CK)) + q;
+          return ok ? __ldg(src) : make_uint4(0u, 0u, 0u, 0u);
+        };
+        auto store_row = [&](int ri, int s, uint4 v) {
+          const int x = ri % cols, rr = ri / cols;
+          const int w = x - s;
+          if (ri >= nrow_items || w < 0 || w >= kTW) return;
+          const int img = rr & 1, hh = rr >> 1;
+          const int rho = hh * (kTI * kTW) + img * kTW + w;
+          st_shared_v4(asm_ + ((it + s) % STAGES) * a_bytes + rho * 128 + ((q ^ (rho & 7)) << 4), v);
+        };
+        const int first = pw * 4 + sub;
+        if (R == 3 && S == 3) {
+          // 3x3 fast path: a warp owns 5 of the 20 (hh, img) rows; lane = (16 B chunk q, column
+          // slot xr) loads columns x = xr, xr + 4, xr + 8 (< 10) of each row, every offset
+          // incremental; stage s receives column x at tile column w = x - s (swizzle q ^ w)
+          constexpr int kRows = 5, kJ = 3;
+          const int xr = sub;
+          uint4 v[kRows][kJ];
 #pragma unroll
-          for (int b = 0; b < kB; ++b) {
-            const int item = base + 4 * b;
-            const int half = item & 1, img = (item >> 1) & 1, hh = item >> 2;
+          for (int i = 0; i < kRows; ++i) {
+            const int rr = pw * kRows + i, img = rr & 1, hh = rr >> 1;
             const int n = np * kTI + img, hi = h0 + hh;
-            const int c0 = ck * CK + (half * 4 + cq) * QV;
-            const bool row_ok = item < items && n < N && hi < H;
-            const int wa = w0 + wl, wb = w0 + wl + 8;
-            const float* src = I + ((static_cast<int64_t>(n) * C + c0) * H + hi) * static_cast<int64_t>(W);
+            const bool row_ok = n < N && hi < H && (ck * CK + q * static_cast<int>(16 / sizeof(T))) < C;
+            const T* rowp = X + ((static_cast<int64_t>(n) * H + hi) * W + w0) * C + ck * CK;
 #pragma unroll
-            for (int j = 0; j < QV; ++j) {
-              const bool cj = row_ok && c0 + j < C;
-              v0[b][j] = (cj && wa < W) ? __ldg(src + j * plane + wa) : 0.0f;
-              v8[b][j] = (cj && wl < S - 1 && wb < W) ? __ldg(src + j * plane + wb) : 0.0f;
+            for (int j = 0; j < kJ; ++j) {
+              const int x = xr + 4 * j;
+              v[i][j] = (row_ok && x < 10 && w0 + x < W)
+                            ? __ldg(reinterpret_cast<const uint4*>(rowp + static_cast<int64_t>(x) * C) + q)
+                            : make_uint4(0u, 0u, 0u, 0u);
             }
           }
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const int k = it + s;
+            const long long tw0 = trace ? clock64() : 0;
+            mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
+            if (trace) pwait += clock64() - tw0;
+            uint8_t* box = asm_ + (k % STAGES) * a_bytes;
+#pragma unroll
+            for (int i = 0; i < kRows; ++i) {
+              const int rr = pw * kRows + i;
+#pragma unroll
+              for (int j = 0; j < kJ; ++j) {
+                const int w = xr + 4 * j - s;
+                if (w >= 0 && w < kTW) st_shared_v4(box + (rr * 8 + w) * 128 + ((q ^ w) << 4), v[i][j]);
+              }
+            }
+            fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+            mbar_arrive(&full[k % STAGES]);
+          }
+        } else {
+          const long long tw0 = trace ? clock64() : 0;
           for (int s = 0; s < S; ++s) {
             const int k = it + s;
-            if (base == pw) {  // first batch: the slot must have been consumed by the MMA
-              const long long tw0 = trace ? clock64() : 0;
-              mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
-              if (trace) pwait += clock64() - tw0;
-            }
-            uint8_t* box = asm_ + (k % STAGES) * a_bytes;
-            const int src_lane = (lane & ~7) | ((wl + s) & 7);
-            const bool lo = wl + s < 8;
-#pragma unroll
-            for (int b = 0; b < kB; ++b) {
-              float v[QV];
-              if (s == 0) {
-#pragma unroll
-                for (int j = 0; j < QV; ++j) v[j] = v0[b][j];
-              } else {
-#pragma unroll
-                for (int j = 0; j < QV; ++j) {
-                  const float x0 = __shfl_sync(0xffffffffu, v0[b][j], src_lane);
-                  const float x8 = __shfl_sync(0xffffffffu, v8[b][j], src_lane);
-                  v[j] = lo ? x0 : x8;
-                }
-              }
-              const int item = base + 4 * b;
-              if (item < items) {
-                const int half = item & 1, img = (item >> 1) & 1, hh = item >> 2;
-                const int q = half * 4 + cq;
-                const int rho = hh * (kTI * kTW) + img * kTW + wl;
-                *reinterpret_cast<uint4*>(box + rho * 128 + ((q ^ (rho & 7)) << 4)) = pack16(v);
-              }
-            }
-            if (one_batch) {  // stage s complete: publish it now
-              fence_proxy_async_smem();
-              mbar_arrive(&full[k % STAGES]);
-            }
+            mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
           }
-        }
-        if (!one_batch) {
-          fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+          if (trace) pwait += clock64() - tw0;
+          for (int base = first; base < nrow_items; base += 16 * 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) v[b] = load_row(base + 16 * b);
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              for (int s = 0; s < S; ++s) store_row(base + 16 * b, s, v[b]);
+          }
+          fence_proxy_async_smem();
           for (int s = 0; s < S; ++s) mbar_arrive(&full[(it + s) % STAGES]);
         }
         if (warp == 0 && lane == 0 && pstage < 20) CONV_TRACE(20 + pstage, clock64());
@@ -298,17 +305,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// K[f][c][r][s] -> W'[r][s][f][c] (K-major B operand rows for the TMA), the primary grid of the
-// programmatic dependent launch pair: it lets the conv grid launch at once.
+// Pre-pass (one launch, the primary grid of the programmatic dependent launch pair):
+//   blocks [0, N*H)      NCHW row (n, h) -> NHWC X[n][h][:][:] through shared memory (coalesced
+//                        reads along w, 16 B writes along c);
+//   blocks [N*H, ...)    K[f][c][r][s] -> W'[r][s][f][c] (K-major B rows for the conv's TMA).
 template <typename T>
-__global__ void __launch_bounds__(256) k_filters_kmajor(const float* __restrict__ K, T* __restrict__ Wt, int F, int C,
-                                                        int RS) {
+__global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ I, const float* __restrict__ K,
+                                                      T* __restrict__ X, T* __restrict__ Wt, int N, int C, int H,
+                                                      int W, int F, int RS) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ float tile[];  // [C][W + 1]
+  const int rows = N * H;
+  if (static_cast<int>(blockIdx.x) < rows) {
+    const int n = blockIdx.x / H, h = blockIdx.x % H;
+    const int pitch = W + 1;
+    const float* src = I + (static_cast<int64_t>(n) * C * H + h) * W;
+    for (int i = threadIdx.x; i < C * W; i += blockDim.x) {
+      const int c = i / W, w = i - c * W;
+      tile[c * pitch + w] = __ldg(src + static_cast<int64_t>(c) * H * W + w);
+    }
+    __syncthreads();
+    T* dst = X + (static_cast<int64_t>(n) * H + h) * W * C;
+    for (int i = threadIdx.x; i < C * W; i += blockDim.x) {
+      const int w = i / C, c = i - w * C;
+      dst[i] = from_f32<T>(tile[c * pitch + w]);
+    }
+    return;
+  }
   const int64_t total = static_cast<int64_t>(F) * C * RS;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // e indexes the source (coalesced reads): e = (f*C + c)*RS + rs
-    const int rs = static_cast<int>(e % RS);
+  const int nb = gridDim.x - rows;
+  for (int64_t e = (blockIdx.x - rows) * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(nb) * blockDim.x) {
+    const int rs = static_cast<int>(e % RS);  // source order: e = (f*C + c)*RS + rs
     const int64_t fc = e / RS;
     const int c = static_cast<int>(fc % C), f = static_cast<int>(fc / C);
     Wt[(static_cast<int64_t>(rs) * F + f) * C + c] = from_f32<T>(__ldg(K + e));
@@ -342,9 +370,15 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
                "conv_tc smem attribute");
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
-    k_filters_kmajor<T><<<static_cast<unsigned>(std::min<int64_t>(a.sms, (wt + 255) / 256)), 256, 0, st>>>(
-        K, static_cast<T*>(a.ws_w), a.F, a.C, a.R * a.S);
-    check_cuda(cudaGetLastError(), "filters_kmajor launch");
+    const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
+    const size_t pre_smem = static_cast<size_t>(a.C) * (a.W + 1) * sizeof(float);
+    check_cuda(cudaFuncSetAttribute(k_conv_prepass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(pre_smem)),
+               "prepass smem attribute");
+    k_conv_prepass<T><<<a.N * a.H + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
+                                                                 static_cast<T*>(a.ws_w), a.N, a.C, a.H, a.W, a.F,
+                                                                 a.R * a.S);
+    check_cuda(cudaGetLastError(), "conv prepass launch");
     count_launch();
     static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
     static long long* trace = nullptr;
@@ -359,7 +393,7 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, I, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a.ws_x), a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
                                   tiles_w, total, trace),
                "conv_tc launch");
     if (trace) {  // developer path: synchronous dump of the last launch
@@ -400,6 +434,10 @@ bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
   const int es = bf16 ? 2 : 4;
   return stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8 &&
          conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256;
+}
+
+bool conv_tc_prepass_fits(int C, int W) {  // one NCHW row of all channels through shared memory
+  return static_cast<size_t>(C) * (W + 1) * sizeof(float) <= 96 * 1024;
 }
 
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {

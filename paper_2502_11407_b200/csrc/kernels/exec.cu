@@ -202,7 +202,8 @@ bool conv_tc_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4) return false;
   return conv_tc_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
                            static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
-                           static_cast<int>(op.stride), bf16);
+                           static_cast<int>(op.stride), bf16) &&
+         conv_tc_prepass_fits(static_cast<int>(op.param("C")), static_cast<int>(op.param("W")));
 }
 
 int resolve_variant(const OpDesc& op, int variant) {
@@ -303,15 +304,18 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.OW = static_cast<int>(op.param("OW"));
           c.bf16 = bf16;
           c.sms = sms;
-          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * (bf16 ? 2 : 4);
-          check_cuda(cudaMalloc(&k->ws, wb), "conv workspace");
+          const size_t es = bf16 ? 2 : 4;
+          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
+          const size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
+          check_cuda(cudaMalloc(&k->ws, ((wb + 255) & ~size_t(255)) + xb), "conv workspace");
           c.ws_w = k->ws;
+          c.ws_x = static_cast<char*>(k->ws) + ((wb + 255) & ~size_t(255));
           k->launches = 2;  // filter conversion + conv (programmatic dependent launch), timed as one span
           k->launch_names = {"conv_tc"};
           const int tiles = ((c.N + 1) / 2) * ((c.OH + 7) / 8) * ((c.OW + 7) / 8);
           pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F
              << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
-             << ",\"block\":416,\"launches\":2,\"im2col\":\"in-kernel from NCHW\",\"filters\":\"K-major conversion launch + PDL\"}";
+             << ",\"block\":416,\"launches\":2,\"im2col\":\"in-kernel from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
         } else {
           throw Error(Code::Unsupported, std::string(kVariantNames[k->variant]) + " not available for " + op.label());
         }

@@ -45,12 +45,14 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
 struct ConvTcArgs {
   CUtensorMap mapW;   // over the W'[r][s][f][c] workspace, built once
   bool maps_ready = false;
-  void* ws_w = nullptr;  // W' workspace, rewritten by the filter-conversion launch of every execute
+  void* ws_w = nullptr;  // W' workspace, rewritten by the pre-pass launch of every execute
+  void* ws_x = nullptr;  // NHWC copy of the input, rewritten by the pre-pass launch
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
   int sms = 148;
   bool bf16 = false;
 };
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
+bool conv_tc_prepass_fits(int C, int W);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
 
