@@ -318,17 +318,48 @@ __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ 
   const int rows = N * H;
   if (static_cast<int>(blockIdx.x) < rows) {
     const int n = blockIdx.x / H, h = blockIdx.x % H;
-    const int pitch = W + 1;
+    const int pitch = W + 1;  // odd pitch: the transposed reads below are bank-conflict free
     const float* src = I + (static_cast<int64_t>(n) * C * H + h) * W;
-    for (int i = threadIdx.x; i < C * W; i += blockDim.x) {
-      const int c = i / W, w = i - c * W;
-      tile[c * pitch + w] = __ldg(src + static_cast<int64_t>(c) * H * W + w);
+    const int cw = C * W;
+    // 16 independent loads in flight per thread before any shared store
+    for (int i0 = threadIdx.x; i0 < cw; i0 += 16 * 256) {
+      float v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int i = i0 + u * 256;
+        const int c = i / W, w = i - c * W;
+        v[u] = i < cw ? __ldg(src + static_cast<int64_t>(c) * H * W + w) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int i = i0 + u * 256;
+        const int c = i / W, w = i - c * W;
+        if (i < cw) tile[c * pitch + w] = v[u];
+      }
     }
     __syncthreads();
     T* dst = X + (static_cast<int64_t>(n) * H + h) * W * C;
-    for (int i = threadIdx.x; i < C * W; i += blockDim.x) {
-      const int w = i / C, c = i - w * C;
-      dst[i] = from_f32<T>(tile[c * pitch + w]);
+    if (C % 4 == 0) {  // 4 consecutive channels of one column per thread: 16 B (fp32) stores
+      const int c4n = C / 4;
+      for (int j = threadIdx.x; j < W * c4n; j += 256) {
+        const int w = j / c4n, c = (j - w * c4n) * 4;
+        const float a0 = tile[c * pitch + w], a1 = tile[(c + 1) * pitch + w];
+        const float a2 = tile[(c + 2) * pitch + w], a3 = tile[(c + 3) * pitch + w];
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<float4*>(dst + static_cast<int64_t>(w) * C + c) = make_float4(a0, a1, a2, a3);
+        } else {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&lo);
+          u.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(dst + static_cast<int64_t>(w) * C + c) = u;
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < cw; i += 256) {
+        const int w = i / C, c = i - w * C;
+        dst[i] = from_f32<T>(tile[c * pitch + w]);
+      }
     }
     return;
   }

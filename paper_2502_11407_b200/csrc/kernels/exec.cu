@@ -30,7 +30,7 @@ void check_cuda(cudaError_t e, const char* what) {
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-enum class Family { Generic, GemmTc, ConvTc, Stream };
+enum class Family { Generic, GemmTc, ConvTc, ConvGemm, Stream };
 
 struct Kernel {
   OpDesc op;
@@ -41,6 +41,7 @@ struct Kernel {
   bool f64 = false;
   GemmTcArgs gemm;
   ConvTcArgs conv;
+  ConvGemmArgs cgemm;
   StreamArgs stream;
   int launches = 1;
   std::vector<std::string> launch_names{"generic_simt"};
@@ -206,11 +207,14 @@ bool conv_tc_ok(const OpDesc& op, bool bf16) {
          conv_tc_prepass_fits(static_cast<int>(op.param("C")), static_cast<int>(op.param("W")));
 }
 
+// General implicit-GEMM conv (tf32): any stride / window / channel count.
+bool conv_gemm_ok(const OpDesc& op, bool bf16) { return op.kind == Kind::Conv2d && op.dtype_bytes == 4 && !bf16; }
+
 int resolve_variant(const OpDesc& op, int variant) {
   if (variant != -1) return variant;
   if (op.kind == Kind::Gemm && op.dtype_bytes == 2 && gemm_tc_ok(op, true)) return 3;
   if (op.kind == Kind::Gemm && gemm_tc_ok(op, false)) return 2;
-  if (op.kind == Kind::Conv2d && conv_tc_ok(op, false)) return 2;
+  if (op.kind == Kind::Conv2d && (conv_tc_ok(op, false) || conv_gemm_ok(op, false))) return 2;
   if (stream_ok(op)) return 4;
   return 1;
 }
@@ -316,6 +320,34 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F
              << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
              << ",\"block\":416,\"launches\":2,\"im2col\":\"in-kernel from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
+        } else if (conv_gemm_ok(op, bf16)) {
+          k->family = Family::ConvGemm;
+          k->launches = 2;  // filter conversion + conv (programmatic dependent launch), one span
+          k->launch_names = {"conv_gemm"};
+          ConvGemmArgs& c = k->cgemm;
+          c.N = static_cast<int>(op.param("N"));
+          c.C = static_cast<int>(op.param("C"));
+          c.H = static_cast<int>(op.param("H"));
+          c.W = static_cast<int>(op.param("W"));
+          c.F = static_cast<int>(op.param("F"));
+          c.R = static_cast<int>(op.ax[5].extent);
+          c.S = static_cast<int>(op.ax[6].extent);
+          c.stride = static_cast<int>(op.stride);
+          c.OH = static_cast<int>(op.ax[2].extent);
+          c.OW = static_cast<int>(op.ax[3].extent);
+          c.sms = sms;
+          // N tile: the schedule's level-1 f tile, clamped to the UMMA range [64, 256] and to F
+          int bn = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, 256));
+          while (bn > 64 && bn / 2 >= c.F) bn /= 2;
+          c.BN = bn;
+          const int Cp = (c.C + 3) / 4 * 4;
+          check_cuda(cudaMalloc(&k->ws, static_cast<size_t>(c.R) * c.S * c.F * Cp * 4), "conv_gemm workspace");
+          c.ws_w = k->ws;
+          const int64_t P = static_cast<int64_t>(c.N) * c.OH * c.OW;
+          const int64_t tiles = ((P + 127) / 128) * ((c.F + bn - 1) / bn);
+          pi << "{\"family\":\"conv_gemm\",\"BM\":128,\"BN\":" << bn << ",\"tiles\":" << tiles
+             << ",\"grid\":" << std::min<int64_t>(tiles, sms)
+             << ",\"block\":416,\"launches\":2,\"A\":\"MN-major im2col from NCHW in place\"}";
         } else {
           throw Error(Code::Unsupported, std::string(kVariantNames[k->variant]) + " not available for " + op.label());
         }
@@ -397,6 +429,9 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
       break;
     case Family::ConvTc:
       launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st, mk);
+      break;
+    case Family::ConvGemm:
+      launch_conv_gemm(k->cgemm, d_in[0], d_in[1], d_out, st, mk);
       break;
     case Family::Stream:
       mk.mark(st);

@@ -51,6 +51,17 @@ struct ConvTcArgs {
   int sms = 148;
   bool bf16 = false;
 };
+// ---- general tensor-core implicit-GEMM conv2d reading NCHW in place (conv_gemm.cu) ----
+struct ConvGemmArgs {
+  CUtensorMap mapW;  // over W'[r][s][f][Cp]
+  bool map_ready = false;
+  void* ws_w = nullptr;  // W' workspace (pre-pass launch of every execute)
+  int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, stride = 1, OH = 0, OW = 0;
+  int BN = 128;
+  int sms = 148;
+};
+void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
+
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 bool conv_tc_prepass_fits(int C, int W);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);

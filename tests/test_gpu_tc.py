@@ -130,3 +130,20 @@ def test_auto_picks_tensor_cores():
         sched = g.optimize(op, hw(), g.EngineConfig(mode="b200", top_k=1))
         k = g.Kernel(op, sched, 0, "auto")
         assert k.info["variant_name"] == "tc_tf32"
+
+
+# General implicit-GEMM conv (conv_gemm: NCHW read in place, any stride / window / channels):
+# the shapes conv_tc does not take — stride 2, ResNet stem (C=3, 7x7), F > 256, odd batch.
+GEMM_CONVS = [
+    {"kind": "conv2d", "I": [2, 16, 17, 17], "K": [32, 16, 3, 3], "S": 2},
+    {"kind": "conv2d", "I": [3, 3, 23, 23], "K": [64, 3, 7, 7], "S": 2},       # stem: C=3 (padded to 4)
+    {"kind": "conv2d", "I": [1, 64, 9, 9], "K": [300, 64, 1, 1], "S": 1},       # F > 256, ragged N tile
+    {"kind": "conv2d", "I": [2, 96, 8, 8], "K": [128, 96, 1, 1], "S": 2},      # 1x1 stride-2 projection
+    {"kind": "conv2d", "I": [1, 512, 9, 9], "K": [64, 512, 3, 3], "S": 1},     # large C: weights streamed
+]
+
+
+@pytest.mark.parametrize("doc", GEMM_CONVS, ids=lambda d: json.dumps(d["I"] + d["K"] + [d["S"]]))
+def test_conv_gemm_tf32(doc):
+    info = check(doc, "tc_tf32", TF32_TOL)
+    assert info["plan"]["family"] == "conv_gemm"
