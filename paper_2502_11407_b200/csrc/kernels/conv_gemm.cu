@@ -36,7 +36,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kGThreads, 1)
     k_conv_gemm(const float* __restrict__ I, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
                 int C, int H, int W, int F, int R, int S, int stride, int OH, int OW, int tiles_m, int tiles_n,
-                int total) {
+                int total, int packed) {
   constexpr int BM = 128, BK = 32;                 // tf32: 32 channels = 128 B per K row
   constexpr uint32_t A_BYTES = BM * BK * 4;        // 4 MN chunks x 4 KB
   constexpr uint32_t B_BYTES = BN * 128;
@@ -47,15 +47,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint8_t* staging = smem + STAGES * STAGE;  // 4 epilogue warps x 32 x 32 fp32
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * 32 * 32 * 4);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nck = (C + BK - 1) / BK;
-  const int nk = R * S * nck;
+  // k-blocks: general mode (r, s, 32-channel chunk); packed mode (few channels, C*S <= 64): per
+  // filter row r the (s, c) pairs form one K axis k = s*C + c, cut into 32-wide blocks
+  const int nck = packed ? (S * C + BK - 1) / BK : (C + BK - 1) / BK;
+  const int nk = packed ? R * nck : R * S * nck;
   const int64_t P = static_cast<int64_t>(N) * OH * OW;
   const int64_t plane = static_cast<int64_t>(H) * W;
 
@@ -91,31 +94,49 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const int oh = rem / OW, ow = rem - oh * OW;
       const float* base = I + static_cast<int64_t>(n) * C * plane + static_cast<int64_t>(oh) * stride * W +
                           static_cast<int64_t>(ow) * stride;
-      for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s)
-          for (int ck = 0; ck < nck; ++ck, ++it) {
-            if ((it & 1) != grp) continue;
-            const int st = it % STAGES;
-            mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-            uint8_t* a_s = smem + st * STAGE;
-            if (pw == 0 && lane == 0) {  // B: BN filters x 32 channels of W'[r][s] (an extra arrival)
-              mbar_arrive_expect_tx(&full[st], B_BYTES);
-              tma_load_3d(a_s + A_BYTES, &mapW, &full[st], ck * BK, nt * BN, r * S + s);
-            }
-            const float* src = base + static_cast<int64_t>(r) * W + s + static_cast<int64_t>(ck) * BK * plane;
-            float v[BK];
+      // k-block kb -> (r, s, channel chunk) [general] or (r, (s,c) chunk) [packed]
+      auto load_kb = [&](int kb, float (&v)[BK]) {
+        if (!packed) {
+          const int ck = kb % nck, rs = kb / nck, r = rs / S, s = rs - r * S;
+          const float* src = base + static_cast<int64_t>(r) * W + s + static_cast<int64_t>(ck) * BK * plane;
 #pragma unroll
-            for (int k = 0; k < BK; ++k)
-              v[k] = (pv && ck * BK + k < C) ? __ldg(src + static_cast<int64_t>(k) * plane) : 0.0f;
-            // MN-major tf32 layout: chunk pw (4 KB) | K row k: (k/4)*512 + (k%4)*128 | granule
-            // (lane/8) ^ (k%4), word lane%8
-            const uint32_t chunk = smem_u32(a_s) + pw * 4096 + (lane & 7) * 4;
+          for (int k = 0; k < BK; ++k)
+            v[k] = (pv && ck * BK + k < C) ? __ldg(src + static_cast<int64_t>(k) * plane) : 0.0f;
+        } else {
+          const int ck = kb % nck, r = kb / nck;
+          const float* src = base + static_cast<int64_t>(r) * W;
 #pragma unroll
-            for (int k = 0; k < BK; ++k)
-              sts32(chunk + (k >> 2) * 512 + (k & 3) * 128 + ((((lane >> 3) ^ (k & 3)) & 3) << 5), v[k]);
-            fence_proxy_async_smem();
-            mbar_arrive(&full[st]);
+          for (int k = 0; k < BK; ++k) {
+            const int kk = ck * BK + k;  // uniform across the warp
+            const int sk = kk / C, c = kk - sk * C;
+            v[k] = (pv && sk < S) ? __ldg(src + static_cast<int64_t>(c) * plane + sk) : 0.0f;
           }
+        }
+      };
+      // this group's k-blocks of the tile: kb = kb0, kb0 + 2, ...
+      const int kb0 = ((it & 1) == grp) ? 0 : 1;
+      for (int kb = kb0; kb < nk; kb += 2) {
+        const int k_it = it + kb;
+        const int st = k_it % STAGES;
+        mbar_wait(&empty[st], ((k_it / STAGES) & 1) ^ 1);
+        uint8_t* a_s = smem + st * STAGE;
+        if (pw == 0 && lane == 0) {  // B: BN filters x 32 K of W' (an extra arrival)
+          const int ck = kb % nck;
+          mbar_arrive_expect_tx(&full[st], B_BYTES);
+          tma_load_3d(a_s + A_BYTES, &mapW, &full[st], ck * BK, nt * BN, kb / nck);
+        }
+        float v[BK];
+        load_kb(kb, v);
+        // MN-major tf32 layout: chunk pw (4 KB) | K row k: (k/4)*512 + (k%4)*128 | granule
+        // (lane/8) ^ (k%4), word lane%8
+        const uint32_t chunk = smem_u32(a_s) + pw * 4096 + (lane & 7) * 4;
+#pragma unroll
+        for (int k = 0; k < BK; ++k)
+          sts32(chunk + (k >> 2) * 512 + (k & 3) * 128 + ((((lane >> 3) ^ (k & 3)) & 3) << 5), v[k]);
+        fence_proxy_async_smem();
+        mbar_arrive(&full[st]);
+      }
+      it += nk;
     }
   } else if (warp == kMma) {
     if (elect_one()) {
@@ -145,25 +166,49 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
   } else {
+    // Epilogue: TMEM lanes (positions) x 32 filters -> the warp's staging rows [f][32 positions]
+    // (conflict-free 4 B stores) -> each lane re-reads 16 B = 4 consecutive positions of one
+    // filter and stores them with one 16 B streaming store: a warp instruction writes 4 filter
+    // rows x 128 B instead of 1 x 128 B. Positions must not straddle an image within a group
+    // of 4 (OH*OW % 4 == 0); otherwise per-element stores.
     const int q = warp & 3;  // TMEM lane quarter = tile rows (positions) 32q .. 32q+31
     const int64_t ohw = static_cast<int64_t>(OH) * OW;
+    float* stg = reinterpret_cast<float*>(staging) + q * (32 * 32);
+    const uint32_t stg_s = smem_u32(stg);
+    const bool vec = (ohw & 3) == 0;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const int mt = t / tiles_n, nt = t % tiles_n;
-      const int64_t p = static_cast<int64_t>(mt) * BM + q * 32 + lane;
-      const int n = static_cast<int>(p / ohw);
-      const int64_t pr = p - n * ohw;
+      const int64_t pw0 = static_cast<int64_t>(mt) * BM + q * 32;  // first position of this warp
+      const int64_t p = pw0 + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
-      float* obase = O + (static_cast<int64_t>(n) * F) * ohw + pr;
+      // vector-store geometry: lane -> (filter row lane/8 of 4, positions 4*(lane%8) .. +3)
+      const int64_t pv4 = pw0 + 4 * (lane & 7);
+      const int n4 = static_cast<int>(pv4 / ohw);
+      const int64_t pr4 = pv4 - n4 * ohw;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (p < P) {
-          const int f0 = nt * BN + c;
+        const int f0 = nt * BN + c;
+        if (vec) {
+          __syncwarp();  // previous chunk's re-reads are done
+#pragma unroll
+          for (int v = 0; v < 32; ++v) sts32(stg_s + (v * 32 + lane) * 4, __uint_as_float(r[v]));
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const int fl = g * 4 + (lane >> 3);
+            const float4 val = *reinterpret_cast<const float4*>(stg + fl * 32 + 4 * (lane & 7));
+            if (pv4 < P && f0 + fl < F)
+              __stcs(reinterpret_cast<float4*>(O + (static_cast<int64_t>(n4) * F + f0 + fl) * ohw + pr4), val);
+          }
+        } else if (p < P) {
+          const int n = static_cast<int>(p / ohw);
+          float* obase = O + (static_cast<int64_t>(n) * F) * ohw + (p - n * ohw);
 #pragma unroll
           for (int v = 0; v < 32; ++v)
             if (f0 + v < F) __stcs(obase + static_cast<int64_t>(f0 + v) * ohw, __uint_as_float(r[v]));
@@ -184,9 +229,23 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 // K[f][c][r][s] -> W'[r][s][f][c] (K-major B rows for the TMA); primary grid of the PDL pair.
 // Rows are padded to Cp = C rounded up to 4 channels (16 B, the TMA stride unit), pad = 0.
+// Packed mode (Cp = S*C rounded up to 4): W'[r][f][s*C + c].
 __global__ void __launch_bounds__(256) k_filters_rsfc(const float* __restrict__ K, float* __restrict__ Wt, int F,
-                                                      int C, int Cp, int RS) {
+                                                      int C, int Cp, int RS, int S, int packed) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (packed) {
+    const int R = RS / S;
+    const int64_t tot = static_cast<int64_t>(R) * F * Cp;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int kk = static_cast<int>(e % Cp);  // e = (r*F + f)*Cp + kk
+      const int64_t rf = e / Cp;
+      const int f = static_cast<int>(rf % F), r = static_cast<int>(rf / F);
+      const int sk = kk / C, c = kk - sk * C;
+      Wt[e] = sk < S ? __ldg(K + ((static_cast<int64_t>(f) * C + c) * R + r) * S + sk) : 0.0f;
+    }
+    return;
+  }
   const int64_t total = static_cast<int64_t>(F) * Cp * RS;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -200,10 +259,11 @@ __global__ void __launch_bounds__(256) k_filters_rsfc(const float* __restrict__ 
 template <int BN>
 void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
   constexpr size_t STAGE = 128 * 128 + BN * 128;
-  constexpr int STAGES = static_cast<int>((227 * 1024 - 2048) / STAGE) >= 4 ? 4 : 3;
+  constexpr int STAGES = static_cast<int>((227 * 1024 - 2048 - 16384) / STAGE) >= 4 ? 4 : 3;
+  const int Cp = a.packed ? (a.S * a.C + 3) / 4 * 4 : (a.C + 3) / 4 * 4;
+  const int planes = a.packed ? a.R : a.R * a.S;
   if (!a.map_ready) {
-    const int Cp = (a.C + 3) / 4 * 4;
-    const uint64_t dw[3] = {static_cast<uint64_t>(Cp), static_cast<uint64_t>(a.F), static_cast<uint64_t>(a.R) * a.S};
+    const uint64_t dw[3] = {static_cast<uint64_t>(Cp), static_cast<uint64_t>(a.F), static_cast<uint64_t>(planes)};
     const uint64_t sw[2] = {static_cast<uint64_t>(Cp) * 4, static_cast<uint64_t>(Cp) * a.F * 4};
     const uint32_t bw[3] = {32, static_cast<uint32_t>(BN), 1};
     encode_map(&a.mapW, false, true, a.ws_w, 3, dw, sw, bw);
@@ -214,14 +274,13 @@ void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cu
   const int total = tiles_m * tiles_n;
   const int grid = std::min(total, a.sms);
   mk.mark(st);
-  const int Cp = (a.C + 3) / 4 * 4;
-  const int64_t wt = static_cast<int64_t>(a.F) * Cp * a.R * a.S;
+  const int64_t wt = static_cast<int64_t>(a.F) * Cp * planes;
   k_filters_rsfc<<<static_cast<unsigned>(std::min<int64_t>(4 * a.sms, (wt + 255) / 256)), 256, 0, st>>>(
-      K, static_cast<float*>(a.ws_w), a.F, a.C, Cp, a.R * a.S);
+      K, static_cast<float*>(a.ws_w), a.F, a.C, Cp, a.R * a.S, a.S, a.packed);
   check_cuda(cudaGetLastError(), "filters_rsfc launch");
   count_launch();
   auto kern = k_conv_gemm<BN, STAGES>;
-  const size_t smem = STAGES * STAGE + 1024 + 256;
+  const size_t smem = STAGES * STAGE + 16384 + 1024 + 256;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
              "conv_gemm smem attribute");
   cudaLaunchConfig_t cfg = {};
@@ -235,7 +294,7 @@ void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cu
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   check_cuda(cudaLaunchKernelEx(&cfg, kern, I, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.stride, a.OH, a.OW,
-                                tiles_m, tiles_n, total),
+                                tiles_m, tiles_n, total, a.packed),
              "conv_gemm launch");
   count_launch();
   mk.mark(st);

@@ -201,6 +201,8 @@ bool gemm_tc_ok(const OpDesc& op, bool bf16) {
 
 bool conv_tc_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4) return false;
+  // conv_tc pays an NHWC pre-pass and wins through filter-row reuse: only for windows (R >= 2)
+  if (op.param("R") < 2 && !bf16) return false;  // (bf16: conv_gemm has no bf16 path)
   return conv_tc_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
                            static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
                            static_cast<int>(op.stride), bf16) &&
@@ -336,18 +338,22 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.OH = static_cast<int>(op.ax[2].extent);
           c.OW = static_cast<int>(op.ax[3].extent);
           c.sms = sms;
-          // N tile: the schedule's level-1 f tile, clamped to the UMMA range [64, 256] and to F
-          int bn = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, 256));
+          // N tile: the schedule's level-1 f tile widened to the UMMA N covering F (<= 256): the
+          // A tile is produced once per N tile, so a wide N tile is what keeps the MMA fed
+          int bn = static_cast<int>(pow2_clamp(std::max<int64_t>(s.L ? s.tile(op, 1, 1) : 128, c.F), 64, 256));
           while (bn > 64 && bn / 2 >= c.F) bn /= 2;
           c.BN = bn;
-          const int Cp = (c.C + 3) / 4 * 4;
-          check_cuda(cudaMalloc(&k->ws, static_cast<size_t>(c.R) * c.S * c.F * Cp * 4), "conv_gemm workspace");
+          c.packed = c.C * c.S <= 64 && c.C < 32;
+          const int Cp = c.packed ? (c.S * c.C + 3) / 4 * 4 : (c.C + 3) / 4 * 4;
+          const size_t planes = c.packed ? c.R : static_cast<size_t>(c.R) * c.S;
+          check_cuda(cudaMalloc(&k->ws, planes * c.F * Cp * 4), "conv_gemm workspace");
           c.ws_w = k->ws;
           const int64_t P = static_cast<int64_t>(c.N) * c.OH * c.OW;
           const int64_t tiles = ((P + 127) / 128) * ((c.F + bn - 1) / bn);
           pi << "{\"family\":\"conv_gemm\",\"BM\":128,\"BN\":" << bn << ",\"tiles\":" << tiles
              << ",\"grid\":" << std::min<int64_t>(tiles, sms)
-             << ",\"block\":416,\"launches\":2,\"A\":\"MN-major im2col from NCHW in place\"}";
+             << ",\"block\":416,\"launches\":2,\"packed_sc\":" << c.packed
+             << ",\"A\":\"MN-major im2col from NCHW in place\"}";
         } else {
           throw Error(Code::Unsupported, std::string(kVariantNames[k->variant]) + " not available for " + op.label());
         }

@@ -58,6 +58,7 @@ struct ConvGemmArgs {
   void* ws_w = nullptr;  // W' workspace (pre-pass launch of every execute)
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, stride = 1, OH = 0, OW = 0;
   int BN = 128;
+  int packed = 0;  // few channels: the (s, c) pairs of a filter row form one K axis
   int sms = 148;
 };
 void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);

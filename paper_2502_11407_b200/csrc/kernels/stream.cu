@@ -681,6 +681,44 @@ __global__ void __launch_bounds__(288) k_window_bulk(const StreamWinArgs a, cons
   }
 }
 
+// Global window (OH = OW = 1: the window covers the whole plane, e.g. ResNet's final 7x7 pool):
+// planes are contiguous, so a CTA stages kGlobalPlanes whole planes with coalesced loads and each
+// thread reduces one plane from shared memory in the interpreter's order (odd plane pitch in
+// words when H*W is odd keeps the per-thread reads conflict-free).
+constexpr int kGlobalPlanes = 256;
+
+template <bool DW>
+__global__ void __launch_bounds__(kGlobalPlanes) k_window_global(const StreamWinArgs a, const float* __restrict__ in,
+                                                                 const float* __restrict__ wts,
+                                                                 float* __restrict__ out) {
+  extern __shared__ float pl[];
+  const int hw = static_cast<int>(a.H * a.W);
+  const float dv = static_cast<float>(a.divisor), y = 1.0f / dv;
+  for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * kGlobalPlanes; g0 < a.planes;
+       g0 += static_cast<int64_t>(gridDim.x) * kGlobalPlanes) {
+    const int np = static_cast<int>(min(static_cast<int64_t>(kGlobalPlanes), a.planes - g0));
+    const float* src = in + g0 * hw;
+    __syncthreads();
+    for (int i = threadIdx.x; i < np * hw; i += kGlobalPlanes) pl[i] = __ldg(src + i);
+    __syncthreads();
+    if (threadIdx.x < np) {
+      const float* p = pl + threadIdx.x * hw;
+      const int64_t plane = g0 + threadIdx.x;
+      const int c = static_cast<int>(plane % a.C);
+      float acc = 0.0f;
+      for (int q = 0; q < a.n_order; ++q) {
+        const int r = a.order[q] >> 4, sx = a.order[q] & 15;
+        const float v = p[r * a.W + sx];
+        if constexpr (DW)
+          acc = fmaf(v, __ldg(wts + c * a.R * a.S + r * a.S + sx), acc);
+        else
+          acc += v;
+      }
+      out[plane] = DW ? acc : div_window(acc, dv, y);
+    }
+  }
+}
+
 template <bool DW, int MODE>
 void run_window(const StreamWinArgs& a, const void* in, const void* w, void* out, cudaStream_t st) {
   const int64_t total_in = a.planes * a.H * a.W;
@@ -784,6 +822,19 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
       w.vec = reinterpret_cast<uintptr_t>(in0) % 16 == 0;
       w.vec_out = (w.OW % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 8 == 0);
       const bool dw = a.kind == StreamKind::DwConv;
+      if (w.OH == 1 && w.OW == 1 && w.H * w.W <= 128) {  // global window over small planes
+        const size_t smem = static_cast<size_t>(kGlobalPlanes) * w.H * w.W * sizeof(float);
+        const int64_t groups = (w.planes + kGlobalPlanes - 1) / kGlobalPlanes;
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, static_cast<int64_t>(w.sms) * 4));
+        auto kern = dw ? k_window_global<true> : k_window_global<false>;
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                   "global window smem attribute");
+        kern<<<grid, kGlobalPlanes, smem, st>>>(w, static_cast<const float*>(in0), static_cast<const float*>(in1),
+                                                static_cast<float*>(out));
+        check_cuda(cudaGetLastError(), "global window launch");
+        count_launch();
+        return;
+      }
       int mode = 0;
       if (w.R == 3 && w.S == 3 && (w.stride == 1 || w.stride == 2) && w.order_kind != 0)
         mode = (w.stride == 1 ? 1 : 3) + (w.order_kind == 2 ? 1 : 0);

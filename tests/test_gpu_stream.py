@@ -41,6 +41,8 @@ OPS = [
     {"kind": "dwconv2d", "I": [2, 6, 19, 21], "K": [6, 1, 3, 3], "S": 2},
     {"kind": "dwconv2d", "I": [1, 5, 12, 13], "K": [5, 1, 5, 5], "S": 1},
     {"kind": "dwconv2d", "I": [2, 16, 114, 114], "K": [16, 1, 3, 3], "S": 1},
+    {"kind": "avgpool2d", "I": [4, 300, 7, 7], "F": 7, "S": 1},               # global pool (ResNet head)
+    {"kind": "dwconv2d", "I": [2, 40, 5, 5], "K": [40, 1, 5, 5], "S": 1},     # global depthwise window
 ]
 
 
