@@ -292,8 +292,13 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           while (bn > 64 && tiles(bn) < sms) bn /= 2;
           g.BN = bn;
           g.sms = sms;
+          // A multicast across clusters of n-tiles when the k-loop is long enough to be
+          // L2-bandwidth bound (each n-tile re-reads the whole A row panel)
+          const int tn = (g.N + bn - 1) / bn, nkb = (g.K * op.dtype_bytes + 127) / 128;
+          g.cs = (nkb >= 8 && tn % 4 == 0 && tiles(bn) >= 4 * 8) ? 4 : (nkb >= 8 && tn % 2 == 0) ? 2 : 1;
           pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
-             << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true}";
+             << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true"
+             << ",\"cluster_n\":" << g.cs << "}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
           k->family = Family::ConvTc;
           k->launches = 1;

@@ -38,7 +38,10 @@ struct TcTraits<__nv_bfloat16> {
 // overlap the MMAs of tile i+1. Epilogue: tcgen05.ld 32 columns -> registers -> the warp's
 // 32-row staging slice in the 128 B-swizzled layout a TMA store expects -> one TMA store per
 // 128 B column block (full-line writes; OOB rows/columns clipped by the tensor map).
-template <typename T, typename TOut, int BN, int STAGES>
+// CS > 1: clusters of CS CTAs along N work on CS horizontally adjacent tiles in lockstep; every
+// CTA TMA-loads 1/CS of the shared A tile and multicasts it to the cluster (A's L2->SM traffic
+// divided by CS), stages are released cluster-wide (multicast tcgen05.commit).
+template <typename T, typename TOut, int BN, int STAGES, int CS>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total) {
@@ -67,11 +70,17 @@ __global__ void __launch_bounds__(192, 1)
   const int lane = threadIdx.x & 31;
   const int nk = (K + BK - 1) / BK;
   const int per_batch = tiles_m * tiles_n;
+  // tile walk: cluster c takes tile groups g = c, c + clusters, ...; rank r of the cluster takes
+  // tile (group's m, group's n * CS + r). CS = 1 is the plain persistent walk.
+  const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cid = blockIdx.x / CS, nclusters = gridDim.x / CS;
+  const int groups = total / CS;
+  auto tile_of = [&](int gi) { return gi * CS + rank; };  // groups hold CS consecutive n-tiles
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // every CTA of the cluster releases each stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -87,13 +96,15 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // peers' barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (elect_one()) {
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int gi = cid; gi < groups; gi += nclusters) {
+        const int t = tile_of(gi);
         const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
         const int m0 = mt * BM, n0 = nt * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -103,7 +114,11 @@ __global__ void __launch_bounds__(192, 1)
           mbar_arrive_expect_tx(&full[s], STAGE);
           uint8_t* a_s = smem + s * STAGE;
           uint8_t* b_s = a_s + A_BYTES;
-          tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
+          if constexpr (CS > 1)  // this CTA's 1/CS row slice of A, to every CTA of the cluster
+            tma_load_3d_mc(a_s + rank * (A_BYTES / CS), &mapA, &full[s], kb * BK, m0 + rank * (BM / CS), b,
+                           static_cast<uint16_t>((1u << CS) - 1));
+          else
+            tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
 #pragma unroll
           for (int j = 0; j < B_CHUNKS; ++j)
             tma_load_3d(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
@@ -113,7 +128,7 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (elect_one()) {
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      for (int gi = cid; gi < groups; gi += nclusters, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -136,7 +151,10 @@ __global__ void __launch_bounds__(192, 1)
             else
               mma_tf32(d, ad, bd, IDESC, (kb | k) != 0);
           }
-          mma_commit(&empty[s]);
+          if constexpr (CS > 1)
+            mma_commit_mc(&empty[s], static_cast<uint16_t>((1u << CS) - 1));
+          else
+            mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[acc]);
       }
@@ -145,7 +163,8 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access = its 32 tile rows
     uint8_t* stg = staging + q * STG_WARP;
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+    for (int gi = cid; gi < groups; gi += nclusters, ++local) {
+      const int t = tile_of(gi);
       const int acc = local & 1;
       const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
       const int m0 = mt * BM, n0 = nt * BN;
@@ -197,6 +216,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);
@@ -215,19 +235,50 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <typename T, typename TOut, int BN, int STAGES>
-void run(const GemmTcArgs& a, cudaStream_t st) {
+template <typename T, typename TOut, int BN, int STAGES, int CS>
+void run_cs(const GemmTcArgs& a, cudaStream_t st) {
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
   const size_t smem = STAGES * STAGE + 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
-  auto kern = k_gemm_tc<T, TOut, BN, STAGES>;
+  auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
              "gemm_tc smem attribute");
   const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + BN - 1) / BN;
   const int total = tiles_m * tiles_n * a.batch;
-  const int grid = std::min(total, a.sms);
-  kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total);
-  check_cuda(cudaGetLastError(), "gemm_tc launch");
+  if constexpr (CS == 1) {
+    const int grid = std::min(total, a.sms);
+    kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total);
+    check_cuda(cudaGetLastError(), "gemm_tc launch");
+  } else {
+    const int grid = std::min(total, a.sms / CS * CS);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total),
+               "gemm_tc cluster launch");
+  }
   count_launch();
+}
+
+// Cluster multicast of A pays when the k-loop is long (A re-read from L2 for every n-tile) and
+// the n-tiles split into whole clusters; CS = cluster size along N.
+template <typename T, typename TOut, int BN, int STAGES>
+void run(const GemmTcArgs& a, cudaStream_t st) {
+  const int tiles_n = (a.N + BN - 1) / BN;
+  if (a.cs == 4 && tiles_n % 4 == 0)
+    run_cs<T, TOut, BN, STAGES, 4>(a, st);
+  else if (a.cs >= 2 && tiles_n % 2 == 0)
+    run_cs<T, TOut, BN, STAGES, 2>(a, st);
+  else
+    run_cs<T, TOut, BN, STAGES, 1>(a, st);
 }
 
 // Pipeline depth: as many stages as fit next to the epilogue staging (227 KB opt-in).
@@ -275,6 +326,10 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
     const uint64_t sa[2] = {static_cast<uint64_t>(a.K) * es, static_cast<uint64_t>(a.K) * a.M * es};
     const uint32_t ba[3] = {bk, 128, 1};
     encode_map(&a.mapA, a.bf16, !a.bf16, A, 3, da, sa, ba);
+    if (a.cs > 1) {  // multicast slices: 128/cs rows per CTA of the cluster
+      const uint32_t bam[3] = {bk, static_cast<uint32_t>(128 / a.cs), 1};
+      encode_map(&a.mapAm, a.bf16, !a.bf16, A, 3, da, sa, bam);
+    }
     const uint64_t db[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.batch)};
     const uint64_t sb[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.K * es};
     const uint32_t bb[3] = {bk, bk, 1};  // 128 B of N x BK rows of K

@@ -31,10 +31,12 @@ void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int ran
 // ---- tensor-core GEMM family (gemm_tc.cu) ----
 struct GemmTcArgs {
   CUtensorMap mapA, mapB, mapC;  // rebuilt when the operand / output pointers change
+  CUtensorMap mapAm;             // A slices for cluster multicast (box rows 128 / cs)
   const void* last_A = nullptr;
   const void* last_B = nullptr;
   void* C = nullptr;
   int M = 0, N = 0, K = 0, batch = 1, BN = 128;
+  int cs = 1;  // cluster size along N (A multicast), 1 = no cluster
   int sms = 148;
   bool bf16 = false;
 };
