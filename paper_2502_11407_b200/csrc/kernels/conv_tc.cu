@@ -309,56 +309,78 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   blocks [0, N*H)      NCHW row (n, h) -> NHWC X[n][h][:][:] through shared memory (coalesced
 //                        reads along w, 16 B writes along c);
 //   blocks [N*H, ...)    K[f][c][r][s] -> W'[r][s][f][c] (K-major B rows for the conv's TMA).
+constexpr int kBandRows = 2;  // pre-pass: input rows per block
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ I, const float* __restrict__ K,
                                                       T* __restrict__ X, T* __restrict__ Wt, int N, int C, int H,
                                                       int W, int F, int RS) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ float tile[];  // [C][W + 1]
-  const int rows = N * H;
+  // one block = a band of kBandRows input rows of one image, all channels: reads C contiguous
+  // runs of kBandRows*W floats (DRAM-page friendly), writes one contiguous NHWC slab
+  const int bands_per_img = (H + kBandRows - 1) / kBandRows;
+  const int rows = N * bands_per_img;
   if (static_cast<int>(blockIdx.x) < rows) {
-    const int n = blockIdx.x / H, h = blockIdx.x % H;
-    const int pitch = W + 1;  // odd pitch: the transposed reads below are bank-conflict free
-    const float* src = I + (static_cast<int64_t>(n) * C * H + h) * W;
-    const int cw = C * W;
-    // 16 independent loads in flight per thread before any shared store
-    for (int i0 = threadIdx.x; i0 < cw; i0 += 16 * 256) {
-      float v[16];
+    const int n = blockIdx.x / bands_per_img, h0 = (blockIdx.x % bands_per_img) * kBandRows;
+    const int nr = min(kBandRows, H - h0);
+    const int run = nr * W;           // floats per channel in this band
+    const int pitch = run + 1;        // odd pitch: transposed reads are bank-conflict free
+    const float* src = I + (static_cast<int64_t>(n) * C * H + h0) * W;
+    const bool v4 = (reinterpret_cast<uintptr_t>(I) & 15) == 0 && run % 4 == 0 &&
+                    (static_cast<int64_t>(H) * W) % 4 == 0 && (static_cast<int64_t>(h0) * W) % 4 == 0;
+    if (v4) {
+      const int r4 = run / 4;
+      for (int i0 = threadIdx.x; i0 < C * r4; i0 += 8 * 256) {
+        float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int i = i0 + u * 256;
-        const int c = i / W, w = i - c * W;
-        v[u] = i < cw ? __ldg(src + static_cast<int64_t>(c) * H * W + w) : 0.0f;
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 256;
+          const int c = i / r4, x = i - c * r4;
+          v[u] = i < C * r4 ? __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(c) * H * W) + x)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 256;
+          const int c = i / r4, x = i - c * r4;
+          if (i < C * r4) {
+            float* t = tile + c * pitch + 4 * x;
+            t[0] = v[u].x;
+            t[1] = v[u].y;
+            t[2] = v[u].z;
+            t[3] = v[u].w;
+          }
+        }
       }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int i = i0 + u * 256;
-        const int c = i / W, w = i - c * W;
-        if (i < cw) tile[c * pitch + w] = v[u];
+    } else {
+      for (int i = threadIdx.x; i < C * run; i += 256) {
+        const int c = i / run, x = i - c * run;
+        tile[c * pitch + x] = __ldg(src + static_cast<int64_t>(c) * H * W + x);
       }
     }
     __syncthreads();
-    T* dst = X + (static_cast<int64_t>(n) * H + h) * W * C;
-    if (C % 4 == 0) {  // 4 consecutive channels of one column per thread: 16 B (fp32) stores
+    T* dst = X + (static_cast<int64_t>(n) * H + h0) * W * C;  // positions x = (h - h0)*W + w
+    if (C % 4 == 0) {  // 4 consecutive channels of one position per thread: 16 B (fp32) stores
       const int c4n = C / 4;
-      for (int j = threadIdx.x; j < W * c4n; j += 256) {
-        const int w = j / c4n, c = (j - w * c4n) * 4;
-        const float a0 = tile[c * pitch + w], a1 = tile[(c + 1) * pitch + w];
-        const float a2 = tile[(c + 2) * pitch + w], a3 = tile[(c + 3) * pitch + w];
+      for (int j = threadIdx.x; j < run * c4n; j += 256) {
+        const int x = j / c4n, c = (j - x * c4n) * 4;
+        const float a0 = tile[c * pitch + x], a1 = tile[(c + 1) * pitch + x];
+        const float a2 = tile[(c + 2) * pitch + x], a3 = tile[(c + 3) * pitch + x];
         if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(dst + static_cast<int64_t>(w) * C + c) = make_float4(a0, a1, a2, a3);
+          *reinterpret_cast<float4*>(dst + static_cast<int64_t>(x) * C + c) = make_float4(a0, a1, a2, a3);
         } else {
           __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
           uint2 u;
           u.x = *reinterpret_cast<uint32_t*>(&lo);
           u.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(dst + static_cast<int64_t>(w) * C + c) = u;
+          *reinterpret_cast<uint2*>(dst + static_cast<int64_t>(x) * C + c) = u;
         }
       }
     } else {
-      for (int i = threadIdx.x; i < cw; i += 256) {
-        const int w = i / C, c = i - w * C;
-        dst[i] = from_f32<T>(tile[c * pitch + w]);
+      for (int i = threadIdx.x; i < C * run; i += 256) {
+        const int x = i / C, c = i - x * C;
+        dst[i] = from_f32<T>(tile[c * pitch + x]);
       }
     }
     return;
@@ -402,11 +424,11 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    const size_t pre_smem = static_cast<size_t>(a.C) * (a.W + 1) * sizeof(float);
+    const size_t pre_smem = static_cast<size_t>(a.C) * (kBandRows * a.W + 1) * sizeof(float);
     check_cuda(cudaFuncSetAttribute(k_conv_prepass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(pre_smem)),
                "prepass smem attribute");
-    k_conv_prepass<T><<<a.N * a.H + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
+    k_conv_prepass<T><<<a.N * ((a.H + kBandRows - 1) / kBandRows) + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
                                                                  static_cast<T*>(a.ws_w), a.N, a.C, a.H, a.W, a.F,
                                                                  a.R * a.S);
     check_cuda(cudaGetLastError(), "conv prepass launch");
@@ -467,8 +489,8 @@ bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
          conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256;
 }
 
-bool conv_tc_prepass_fits(int C, int W) {  // one NCHW row of all channels through shared memory
-  return static_cast<size_t>(C) * (W + 1) * sizeof(float) <= 96 * 1024;
+bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channels through smem
+  return static_cast<size_t>(C) * (kBandRows * W + 1) * sizeof(float) <= 96 * 1024;
 }
 
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {

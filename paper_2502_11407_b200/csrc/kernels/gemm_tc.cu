@@ -7,6 +7,10 @@
 //               tcgen05.commit frees each ring slot and finally signals the epilogue;
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns -> registers -> global (fp32 or bf16).
 #include <cuda_bf16.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cudaTypedefs.h>
 
 #include "../host/error.hpp"
@@ -44,7 +48,10 @@ struct TcTraits<__nv_bfloat16> {
 template <typename T, typename TOut, int BN, int STAGES, int CS>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total) {
+              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
+              long long* __restrict__ trace) {
+#define GEMM_TRACE(slot, v) \
+  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int BM = 128;
   constexpr int BK = 128 / sizeof(T);           // K elements per 128 B swizzle row
   constexpr uint32_t A_BYTES = BM * 128;
@@ -103,6 +110,8 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (elect_one()) {
       int it = 0;
+      long long pw = 0;
+      GEMM_TRACE(10, clock64());
       for (int gi = cid; gi < groups; gi += nclusters) {
         const int t = tile_of(gi);
         const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
@@ -110,7 +119,10 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
+          const long long w0 = trace ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
+          if (trace) pw += clock64() - w0;
+          if (it < 40) GEMM_TRACE(20 + it, clock64());
           mbar_arrive_expect_tx(&full[s], STAGE);
           uint8_t* a_s = smem + s * STAGE;
           uint8_t* b_s = a_s + A_BYTES;
@@ -119,15 +131,19 @@ __global__ void __launch_bounds__(192, 1)
                            static_cast<uint16_t>((1u << CS) - 1));
           else
             tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
+          (void)0;
 #pragma unroll
           for (int j = 0; j < B_CHUNKS; ++j)
             tma_load_3d(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
         }
       }
+      GEMM_TRACE(61, pw);
     }
   } else if (warp == 1) {
     if (elect_one()) {
       int it = 0, local = 0;
+      long long fw = 0;
+      GEMM_TRACE(0, clock64());
       for (int gi = cid; gi < groups; gi += nclusters, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
@@ -135,7 +151,9 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t d = tmem + acc * ACC_COLS;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
+          const long long w0 = trace ? clock64() : 0;
           mbar_wait(&full[s], (it / STAGES) & 1);
+          if (trace) fw += clock64() - w0;
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * STAGE);
           const uint32_t b_addr = a_addr + A_BYTES;
@@ -157,7 +175,9 @@ __global__ void __launch_bounds__(192, 1)
             mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[acc]);
+        if (local < 4) GEMM_TRACE(1 + local, clock64());
       }
+      GEMM_TRACE(60, fw);
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access = its 32 tile rows
@@ -211,8 +231,10 @@ __global__ void __launch_bounds__(192, 1)
         }
         bulk_commit();
       }
+      if (warp == 2 && lane == 0 && local < 4) GEMM_TRACE(6 + local, clock64());
     }
     if (lane == 0) bulk_wait<0>();
+    if (warp == 2 && lane == 0) GEMM_TRACE(9, clock64());
   }
   tc_fence_before();
   __syncthreads();
@@ -246,8 +268,19 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
   const int total = tiles_m * tiles_n * a.batch;
   if constexpr (CS == 1) {
     const int grid = std::min(total, a.sms);
-    kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total);
+    static const char* trace_path = std::getenv("GENSOR_GEMM_TRACE");
+    static long long* trace = nullptr;
+    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
+    kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total, trace);
     check_cuda(cudaGetLastError(), "gemm_tc launch");
+    if (trace) {  // developer path: synchronous dump of the last launch
+      std::vector<long long> h(static_cast<size_t>(grid) * 64);
+      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
+      if (FILE* f = std::fopen(trace_path, "w")) {
+        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
+        std::fclose(f);
+      }
+    }
   } else {
     const int grid = std::min(total, a.sms / CS * CS);
     cudaLaunchConfig_t cfg = {};
@@ -262,7 +295,8 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total),
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total,
+                                  static_cast<long long*>(nullptr)),
                "gemm_tc cluster launch");
   }
   count_launch();
@@ -289,7 +323,9 @@ void run_bn(const GemmTcArgs& a, cudaStream_t st) {
   constexpr int MAXS = static_cast<int>((227 * 1024 - 2048 - STG) / STAGE);
   static_assert(MAXS >= 2, "gemm_tc tile does not fit shared memory");
   const int nk = (a.K + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T));
-  if (MAXS >= 6 && nk > 4)
+  if (MAXS >= 8 && nk > 8)
+    run<T, TOut, BN, 8>(a, st);
+  else if (MAXS >= 6 && nk > 4)
     run<T, TOut, BN, 6>(a, st);
   else if (MAXS >= 4)
     run<T, TOut, BN, 4>(a, st);
