@@ -489,6 +489,52 @@ def sequence_line(args, res, ws, peaks, tf32, clk, total_ms, e2e_ms):
     }
 
 
+def run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, local, pg, barrier):
+    """--workload suite: the independent operator suite (BASELINE configs[0..3]) dealt to the ranks
+    by LPT on the engine's B200 cost estimate (paper_2502_11407_b200/shard.py); each rank runs its
+    share; value = total suite FLOPs / (max over ranks of the summed device time)."""
+    from paper_2502_11407_b200 import shard
+
+    names = ["conv2d"] + SUITE_DEFAULT
+    docs = [WORKLOADS[n]["op"] for n in names]
+    parts = shard.suite_partition(docs, hw, ws)
+    mine = parts[rank]
+    results, total_ms = {}, 0.0
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in mine:
+            spec = WORKLOADS[names[i]]
+            r = run_op(g, torch, spec, hw, args.steps, args.warmup, device, "auto", flush, e2e=False)
+            ms = statistics.mean(r["step_ms"])
+            total_ms += ms
+            results[names[i]] = {"ms": ms, "flops": r["flops"], "bytes": r["bytes"], "rank": rank,
+                                 "variant": r["kernel"].info["variant_name"]}
+    barrier()
+    all_res = [results]
+    t = total_ms
+    if pg:
+        t_t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+        pg.all_reduce(t_t, op=pg.ReduceOp.MAX)
+        t = t_t.item()
+        all_res = [None] * ws
+        pg.all_gather_object(all_res, results)
+    if rank == 0:
+        merged = {k: v for d in all_res for k, v in d.items()}
+        flops = sum(v["flops"] for v in merged.values())
+        line = {"metric": METRIC, "value": flops / (t / 1e3) / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "per op (tf32 / bf16 / f32)",
+                "data": "synthetic U(-1,1)",
+                "config": {"workload": "operator suite (configs[0..3]) LPT-partitioned over GPUs",
+                           "partition": [[names[i] for i in p] for p in parts],
+                           "parallelism": f"{ws} GPU(s), one process per GPU, no collective"},
+                "per_op": merged, "clocks": clk.summary(), "roofline": None, "e2e": None,
+                "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
 def run_ours(args):
     import torch
 
@@ -513,6 +559,10 @@ def run_ours(args):
         if pg:
             pg.barrier()
         torch.cuda.synchronize(device)
+
+    if args.workload == "suite":
+        run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, local, pg, barrier)
+        return
 
     if args.workload in SEQUENCE_NAMES:
         barrier()
@@ -619,7 +669,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(SEQUENCE_NAMES), default="conv2d")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(SEQUENCE_NAMES) + ["suite"], default="conv2d")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
     ap.add_argument("--no-cpu-baseline", action="store_true")
