@@ -160,6 +160,13 @@ int gensor_execute_host(gensor_kernel* k, const void* const* h_inputs, int n_inp
                         void* stream);
 void gensor_kernel_free(gensor_kernel* k);
 
+/* On-device re-ranking of the constructed top-k (the paper profiles its top
+ * candidates on hardware, the reference ranks by the analytical estimate_cost only, engine.cpp:
+ * 179-190): instantiates every complete result of `s` with `variant`, times `iters` executes on
+ * the caller's device buffers and writes {"ms":[...],"order":[...],"best":i} (fastest first). */
+int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, const void* const* d_inputs,
+                  int n_inputs, void* d_output, void* stream, int iters, char* buf, size_t cap, size_t* need);
+
 /* Per-launch device timing (CUDA events recorded on the execute stream around every internal
  * launch). While enabled, gensor_kernel_timings() returns the durations of the LAST execute's
  * launches in ms (synchronising on its events) and their names as a JSON array in `names`. */

@@ -21,6 +21,7 @@ from .gensor import (  # noqa: F401
     launch_count,
     optimize,
     record_probability,
+    rerank,
     state_eval,
     vthread_conflict_ratio,
 )

@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI of the gensor-b200 host library (include/gensor_b200.h). Every entry point catches
 // gb::Error / std::exception and turns it into a status code + thread-local message.
 #include "gensor_b200.h"
@@ -427,6 +428,37 @@ int gensor_execute_host(gensor_kernel* k, const void* const* h_in, int n_in, voi
   return guarded([&]() -> int {
     gb::dev::execute_host(k->k, h_in, n_in, h_out, stream);
     return GENSOR_OK;
+  });
+}
+
+int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, const void* const* d_in, int n_in,
+                  void* d_out, void* stream, int iters, char* buf, size_t cap, size_t* need) {
+  if (!op || !s || !d_out || (n_in > 0 && !d_in)) return fail(GENSOR_EINVALID, "null argument");
+  return guarded([&]() -> int {
+    std::vector<std::pair<float, int>> t;
+    std::ostringstream os;
+    os << "{\"ms\":[";
+    for (size_t i = 0; i < s->results.size(); ++i) {
+      const gb::Sched& st = s->results[i].state;
+      float ms = -1.f;
+      if (st.complete()) {
+        gb::dev::Kernel* k = gb::dev::prepare(op->op, st, variant);
+        try {
+          ms = gb::dev::time_execute(k, d_in, n_in, d_out, stream, iters);
+        } catch (...) {
+          gb::dev::destroy(k);
+          throw;
+        }
+        gb::dev::destroy(k);
+        t.emplace_back(ms, static_cast<int>(i));
+      }
+      os << (i ? "," : "") << gb::json::num(ms);
+    }
+    std::stable_sort(t.begin(), t.end());  // ties keep the analytical order
+    os << "],\"order\":[";
+    for (size_t i = 0; i < t.size(); ++i) os << (i ? "," : "") << t[i].second;
+    os << "],\"best\":" << (t.empty() ? -1 : t[0].second) << "}";
+    return emit(os.str(), buf, cap, need);
   });
 }
 

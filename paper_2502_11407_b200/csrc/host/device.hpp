@@ -23,6 +23,7 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
 void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, void* stream);
 
 void set_timing(Kernel* k, bool on);
+float time_execute(Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream, int iters);
 std::vector<std::pair<std::string, float>> timings(Kernel* k);  // last execute, per launch (ms)
 
 DeviceLimits query(int device);  // cudaGetDeviceProperties -> limits (peaks filled by caller)

@@ -455,6 +455,30 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
   k->marks_used = mk.next;
 }
 
+// Median device time (ms) of `iters` executes, CUDA events on `stream` around each one (after one
+// untimed warm-up execute). Used by the on-device re-ranking of the top-k schedules.
+float time_execute(Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream, int iters) {
+  auto st = static_cast<cudaStream_t>(stream);
+  execute(k, d_in, n_in, d_out, stream);
+  cudaEvent_t a, b;
+  check_cuda(cudaEventCreate(&a), "cudaEventCreate");
+  check_cuda(cudaEventCreate(&b), "cudaEventCreate");
+  std::vector<float> ms;
+  for (int i = 0; i < std::max(1, iters); ++i) {
+    check_cuda(cudaEventRecord(a, st), "cudaEventRecord");
+    execute(k, d_in, n_in, d_out, stream);
+    check_cuda(cudaEventRecord(b, st), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(b), "cudaEventSynchronize");
+    float t = 0.f;
+    check_cuda(cudaEventElapsedTime(&t, a, b), "cudaEventElapsedTime");
+    ms.push_back(t);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  std::sort(ms.begin(), ms.end());
+  return ms[ms.size() / 2];
+}
+
 void set_timing(Kernel* k, bool on) {
   if (on && !k->ev[0])
     for (auto& e : k->ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");

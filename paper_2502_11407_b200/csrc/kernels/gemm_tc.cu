@@ -45,7 +45,7 @@ struct TcTraits<__nv_bfloat16> {
 // CS > 1: clusters of CS CTAs along N work on CS horizontally adjacent tiles in lockstep; every
 // CTA TMA-loads 1/CS of the shared A tile and multicasts it to the cluster (A's L2->SM traffic
 // divided by CS), stages are released cluster-wide (multicast tcgen05.commit).
-template <typename T, typename TOut, int BN, int STAGES, int CS>
+template <typename T, typename TOut, int BN, int STAGES, int CS, int SB>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* staging = smem + STAGES * STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * STG_WARP);
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * SB * STG_WARP);  // SB slices per warp
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access = its 32 tile rows
-    uint8_t* stg = staging + q * STG_WARP;
+    // SB = 2: the warp alternates two staging slices, so tile i+1 is written while tile i's TMA
+    // stores still read (short k-loops: the epilogue is the critical path)
     int local = 0;
     for (int gi = cid; gi < groups; gi += nclusters, ++local) {
       const int t = tile_of(gi);
@@ -190,7 +191,8 @@ __global__ void __launch_bounds__(192, 1)
       const int m0 = mt * BM, n0 = nt * BN;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
-      if (lane == 0) bulk_wait_read<0>();  // the previous tile's TMA stores have read the slice
+      uint8_t* stg = staging + (q * SB + (local % SB)) * STG_WARP;
+      if (lane == 0) bulk_wait_read<SB - 1>();  // the stores that last read this slice are done
       __syncwarp();
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -257,11 +259,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <typename T, typename TOut, int BN, int STAGES, int CS>
+template <typename T, typename TOut, int BN, int STAGES, int CS, int SB = 1>
 void run_cs(const GemmTcArgs& a, cudaStream_t st) {
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
-  const size_t smem = STAGES * STAGE + 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
-  auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS>;
+  const size_t smem = STAGES * STAGE + SB * 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
+  auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS, SB>;
   check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
              "gemm_tc smem attribute");
   const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + BN - 1) / BN;
@@ -307,6 +309,15 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
 template <typename T, typename TOut, int BN, int STAGES>
 void run(const GemmTcArgs& a, cudaStream_t st) {
   const int tiles_n = (a.N + BN - 1) / BN;
+  constexpr size_t STAGE = 128 * 128 + BN * 128;
+  constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
+  const int nk = (a.K + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T));
+  if constexpr (2 * STAGE + 2 * STG + 2048 <= 227 * 1024) {
+    if (nk <= 2 && a.cs == 1) {  // epilogue-bound: double-buffered staging, 2 pipeline stages
+      run_cs<T, TOut, BN, 2, 1, 2>(a, st);
+      return;
+    }
+  }
   if (a.cs == 4 && tiles_n % 4 == 0)
     run_cs<T, TOut, BN, STAGES, 4>(a, st);
   else if (a.cs >= 2 && tiles_n % 2 == 0)

@@ -100,6 +100,7 @@ def _load() -> ctypes.CDLL:
         "gensor_launch_count": (ctypes.c_uint64, []),
         "gensor_kernel_set_timing": (I, [P, I]),
         "gensor_kernel_timings": (I, [P, ctypes.POINTER(ctypes.c_float), I, IP, ctypes.c_char_p, SZ]),
+        "gensor_rerank": (I, [P, P, I, PP, I, P, P, I, ctypes.c_char_p, SZ, SZP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -118,6 +119,7 @@ EXPORTED = [
     "gensor_anneal_cache_multiplier", "gensor_record_probability", "gensor_derive_seed",
     "gensor_kernel_prepare", "gensor_kernel_info", "gensor_execute", "gensor_execute_host",
     "gensor_kernel_free", "gensor_launch_count", "gensor_kernel_set_timing", "gensor_kernel_timings",
+    "gensor_rerank",
 ]
 
 
@@ -356,6 +358,17 @@ def derive_seed(seed: int, restart: int) -> int:
 
 def launch_count() -> int:
     return _lib.gensor_launch_count()
+
+
+def rerank(op: "TensorOpSpec", schedules: "Schedules", inputs: Sequence[Any], output: Any,
+           variant: str | int = "auto", iters: int = 5, stream: Any = None) -> dict:
+    """On-device re-ranking of the constructed top-k: every result of
+    ``schedules`` is instantiated with ``variant`` and timed on the given device buffers.
+    Returns {"ms": [...per result...], "order": [fastest first], "best": index}."""
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    ptrs = (ctypes.c_void_p * max(1, len(inputs)))(*[_ptr(t) for t in inputs])
+    return _json_call(_lib.gensor_rerank, op._h, schedules._h, v, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
+                      ctypes.c_void_p(_stream(stream)), iters)
 
 
 class Kernel:

@@ -170,3 +170,23 @@ def test_execute_host_matches_device():
     out = np.empty(ref.size, dtype=np.float32)
     k.execute_host(xs, out)
     assert np.array_equal(out.astype(np.float64), ref)
+
+
+def test_rerank_on_device_orders_by_measured_time():
+    """the top-k schedules are instantiated and timed on the device; the
+    returned order is by measured time and every variant's result stays bit-exact."""
+    doc = {"kind": "gemm", "M": 256, "K": 128, "N": 192}
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=4))
+    rng = np.random.default_rng(7)
+    _, xs = _inputs(doc, rng, integer=True)
+    dev = _to_dev(xs, False)
+    out = torch.empty(256 * 192, device="cuda")
+    r = g.rerank(op, sched, dev, out, "simt_f32", iters=3)
+    assert sorted(r["order"]) == list(range(len(sched)))
+    ms = [r["ms"][i] for i in r["order"]]
+    assert ms == sorted(ms) and all(m > 0 for m in ms)
+    best = r["best"]
+    ref = _round(O.reference_compute(doc, xs), False)
+    got = _run(op, sched, best, "simt_f32", xs, ref.size)
+    assert np.array_equal(got, ref)
