@@ -25,7 +25,8 @@ namespace {
 
 using namespace tc;
 
-constexpr int kGProducerWarps = 8;  // two groups of 4: group g fills k-blocks kb = g (mod 2)
+constexpr int kGGroups = 3;                    // producer groups: group g fills k-blocks kb = g (mod 3)
+constexpr int kGProducerWarps = 4 * kGGroups;  // 4 warps (one 32-position MN chunk each) per group
 constexpr int kGThreads = 32 * (kGProducerWarps + 1 + 4);
 
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
@@ -113,9 +114,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
           }
         }
       };
-      // this group's k-blocks of the tile: kb = kb0, kb0 + 2, ...
-      const int kb0 = ((it & 1) == grp) ? 0 : 1;
-      for (int kb = kb0; kb < nk; kb += 2) {
+      // this group's k-blocks of the tile: global k-block counter it + kb = grp (mod kGGroups)
+      const int kb0 = ((grp - it) % kGGroups + kGGroups) % kGGroups;
+      for (int kb = kb0; kb < nk; kb += kGGroups) {
         const int k_it = it + kb;
         const int st = k_it % STAGES;
         mbar_wait(&empty[st], ((k_it / STAGES) & 1) ^ 1);
