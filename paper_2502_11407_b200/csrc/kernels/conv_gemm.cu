@@ -25,7 +25,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int kGGroups = 3;                    // producer groups: group g fills k-blocks kb = g (mod 3)
+constexpr int kGGroups = 4;                    // producer groups: group g fills k-blocks kb = g (mod 4)
 constexpr int kGProducerWarps = 4 * kGGroups;  // 4 warps (one 32-position MN chunk each) per group
 constexpr int kGThreads = 32 * (kGProducerWarps + 1 + 4);
 
