@@ -187,12 +187,11 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
     rng.manual_seed(0)
     xs, out = make_inputs(op, spec, rng, torch, device)
     stream = torch.cuda.current_stream(device)
-    if timing:
-        k.set_timing(True)
     for _ in range(warmup):
         k.execute(xs, out, stream)
     torch.cuda.synchronize(device)
 
+    # timed steps: no instrumentation inside the events
     step_ms, launch_ms = [], {}
     n0 = g.launch_count()
     for _ in range(steps):
@@ -204,10 +203,17 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
         e.record(stream)
         e.synchronize()
         step_ms.append(s.elapsed_time(e))
-        if timing:
+    launches = g.launch_count() - n0
+    # per-launch breakdown (roofline): separate pass with events around every internal launch
+    if timing:
+        k.set_timing(True)
+        for _ in range(max(3, steps // 2)):
+            if flush is not None:
+                flush.zero_()
+            k.execute(xs, out, stream)
             for name, ms in k.timings():
                 launch_ms.setdefault(name, []).append(ms)
-    launches = g.launch_count() - n0
+        k.set_timing(False)
     res = dict(op=op, kernel=k, sched=sched, step_ms=step_ms, launch_ms=launch_ms, launches=launches,
                construct_s=statistics.median(con), flops=op.flops, bytes=op.bytes)
     if e2e:

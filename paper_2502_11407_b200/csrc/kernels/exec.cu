@@ -298,9 +298,29 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           static const int cs_env = std::getenv("GENSOR_GEMM_CLUSTER") ? std::atoi(std::getenv("GENSOR_GEMM_CLUSTER")) : 1;
           const int tn = (g.N + bn - 1) / bn;
           g.cs = (cs_env >= 4 && tn % 4 == 0) ? 4 : (cs_env >= 2 && tn % 2 == 0) ? 2 : 1;
+          // split-K (GENSOR_GEMM_SPLITK=1) for fp32 output when the tile grid leaves half the SMs
+          // idle: BN 128 tiles x k-splits, partials added by the tile's owner in a fixed order.
+          // Measured slower on G (22.5 vs 15.3 us: the owner's partial reads are latency bound),
+          // so off by default.
+          static const bool splitk_env = std::getenv("GENSOR_GEMM_SPLITK") != nullptr;
+          const int nkb = (g.K * op.dtype_bytes + 127) / 128;
+          if (splitk_env && !bf16 && g.cs == 1 && nkb >= 16) {
+            const int64_t t128 = static_cast<int64_t>((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+            int sp = 1;
+            while (sp < 4 && t128 * sp * 2 <= sms && nkb / (sp * 2) >= 8) sp *= 2;
+            if (sp > 1) {
+              g.BN = 128;
+              g.splits = sp;
+              const size_t pb = static_cast<size_t>(t128) * (sp - 1) * 128 * 128 * 4;
+              check_cuda(cudaMalloc(&k->ws, pb + static_cast<size_t>(t128) * 8), "gemm split-K workspace");
+              g.partials = static_cast<float*>(k->ws);
+              g.flags = reinterpret_cast<unsigned long long*>(static_cast<char*>(k->ws) + pb);
+              check_cuda(cudaMemset(g.flags, 0, static_cast<size_t>(t128) * 8), "gemm split-K flags");
+            }
+          }
           pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
              << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true"
-             << ",\"cluster_n\":" << g.cs << "}";
+             << ",\"cluster_n\":" << g.cs << ",\"split_k\":" << g.splits << "}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
           k->family = Family::ConvTc;
           k->launches = 1;

@@ -49,7 +49,8 @@ template <typename T, typename TOut, int BN, int STAGES, int CS, int SB>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
-              long long* __restrict__ trace) {
+              long long* __restrict__ trace, int splits, float* __restrict__ partials,
+              unsigned long long* __restrict__ flags, unsigned long long flag_target) {
 #define GEMM_TRACE(slot, v) \
   if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int BM = 128;
@@ -81,8 +82,13 @@ __global__ void __launch_bounds__(192, 1)
   // tile (group's m, group's n * CS + r). CS = 1 is the plain persistent walk.
   const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int cid = blockIdx.x / CS, nclusters = gridDim.x / CS;
-  const int groups = total / CS;
-  auto tile_of = [&](int gi) { return gi * CS + rank; };  // groups hold CS consecutive n-tiles
+  // split-K (splits > 1, CS == 1): work unit = (tile, k-split); the units of splits S-1..1 come
+  // first and the owners (split 0, which add the partials and store C) last, so an owner only
+  // ever waits on units that are running or done — never on one queued behind it
+  const int groups = total / CS * splits;
+  auto tile_of = [&](int gi) { return (gi % (total / CS)) * CS + rank; };
+  auto split_of = [&](int gi) { return splits - 1 - gi / (total / CS); };
+  auto kb_lo = [&](int sp) { return static_cast<int>(static_cast<int64_t>(nk) * sp / splits); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -113,10 +119,10 @@ __global__ void __launch_bounds__(192, 1)
       long long pw = 0;
       GEMM_TRACE(10, clock64());
       for (int gi = cid; gi < groups; gi += nclusters) {
-        const int t = tile_of(gi);
+        const int t = tile_of(gi), sp = split_of(gi);
         const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
         const int m0 = mt * BM, n0 = nt * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           const long long w0 = trace ? clock64() : 0;
@@ -149,7 +155,8 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int sp = split_of(gi), kb0 = kb_lo(sp);
+        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
           const int s = it % STAGES;
           const long long w0 = trace ? clock64() : 0;
           mbar_wait(&full[s], (it / STAGES) & 1);
@@ -165,9 +172,9 @@ __global__ void __launch_bounds__(192, 1)
                                     ? smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 1024, 2)
                                     : smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 512, 1);
             if constexpr (TcTraits<T>::kF16Kind)
-              mma_f16(d, ad, bd, IDESC, (kb | k) != 0);
+              mma_f16(d, ad, bd, IDESC, ((kb - kb0) | k) != 0);
             else
-              mma_tf32(d, ad, bd, IDESC, (kb | k) != 0);
+              mma_tf32(d, ad, bd, IDESC, ((kb - kb0) | k) != 0);
           }
           if constexpr (CS > 1)
             mma_commit_mc(&empty[s], static_cast<uint16_t>((1u << CS) - 1));
@@ -185,12 +192,46 @@ __global__ void __launch_bounds__(192, 1)
     // stores still read (short k-loops: the epilogue is the critical path)
     int local = 0;
     for (int gi = cid; gi < groups; gi += nclusters, ++local) {
-      const int t = tile_of(gi);
+      const int t = tile_of(gi), sp = split_of(gi);
       const int acc = local & 1;
       const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
       const int m0 = mt * BM, n0 = nt * BN;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
+      if (sp > 0) {  // split-K partner: this warp's 32 rows of the partial tile -> workspace
+        if constexpr (sizeof(TOut) == 4) {
+          float* prow = partials + ((static_cast<int64_t>(t) * (splits - 1) + sp - 1) * BM + q * 32 + lane) * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<uint4*>(prow + c + 4 * k) = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+          }
+          tc_fence_before();
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&acc_empty[acc]);
+            atomicAdd(&flags[t], 1ULL);  // 4 warps x (splits - 1) partners publish per tile
+          }
+        }
+        continue;
+      }
+      float part_scale = splits > 1 ? 1.0f : 0.0f;  // owner: add the partner splits' partials
+      if (splits > 1) {
+        if (lane == 0)
+          while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + t) : "memory");
+            if (v >= flag_target) break;
+            __nanosleep(64);
+          }
+        __syncwarp();
+        __threadfence();
+      }
       uint8_t* stg = staging + (q * SB + (local % SB)) * STG_WARP;
       if (lane == 0) bulk_wait_read<SB - 1>();  // the stores that last read this slice are done
       __syncwarp();
@@ -199,6 +240,20 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[32];
         tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
+        if (part_scale != 0.0f) {  // fixed order: split 1, 2, ... (deterministic)
+          for (int sp2 = 1; sp2 < splits; ++sp2) {
+            const float* prow =
+                partials + ((static_cast<int64_t>(t) * (splits - 1) + sp2 - 1) * BM + q * 32 + lane) * BN + c;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float4 pv = __ldcg(reinterpret_cast<const float4*>(prow) + k);
+              r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + pv.x);
+              r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + pv.y);
+              r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + pv.z);
+              r[4 * k + 3] = __float_as_uint(__uint_as_float(r[4 * k + 3]) + pv.w);
+            }
+          }
+        }
         if constexpr (sizeof(TOut) == 4) {  // 32 fp32 = one 128 B block, 8 chunks
           uint8_t* blk = stg + (c / 32) * (32 * 128) + lane * 128;
 #pragma unroll
@@ -260,7 +315,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <typename T, typename TOut, int BN, int STAGES, int CS, int SB = 1>
-void run_cs(const GemmTcArgs& a, cudaStream_t st) {
+void run_cs(GemmTcArgs& a, cudaStream_t st) {
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
   const size_t smem = STAGES * STAGE + SB * 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
   auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS, SB>;
@@ -273,7 +328,11 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
     static const char* trace_path = std::getenv("GENSOR_GEMM_TRACE");
     static long long* trace = nullptr;
     if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
-    kern<<<grid, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total, trace);
+    const int units = total * a.splits;
+    const int grid_u = std::min(units, a.sms);
+    if (a.splits > 1) a.flag_target += 4ULL * (a.splits - 1);
+    kern<<<grid_u, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total, trace, a.splits,
+                                    a.partials, a.flags, a.flag_target);
     check_cuda(cudaGetLastError(), "gemm_tc launch");
     if (trace) {  // developer path: synchronous dump of the last launch
       std::vector<long long> h(static_cast<size_t>(grid) * 64);
@@ -298,7 +357,8 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total,
-                                  static_cast<long long*>(nullptr)),
+                                  static_cast<long long*>(nullptr), 1, static_cast<float*>(nullptr),
+                                  static_cast<unsigned long long*>(nullptr), 0ULL),
                "gemm_tc cluster launch");
   }
   count_launch();
@@ -307,7 +367,7 @@ void run_cs(const GemmTcArgs& a, cudaStream_t st) {
 // Cluster multicast of A pays when the k-loop is long (A re-read from L2 for every n-tile) and
 // the n-tiles split into whole clusters; CS = cluster size along N.
 template <typename T, typename TOut, int BN, int STAGES>
-void run(const GemmTcArgs& a, cudaStream_t st) {
+void run(GemmTcArgs& a, cudaStream_t st) {
   const int tiles_n = (a.N + BN - 1) / BN;
   constexpr size_t STAGE = 128 * 128 + BN * 128;
   constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
@@ -328,7 +388,7 @@ void run(const GemmTcArgs& a, cudaStream_t st) {
 
 // Pipeline depth: as many stages as fit next to the epilogue staging (227 KB opt-in).
 template <typename T, typename TOut, int BN>
-void run_bn(const GemmTcArgs& a, cudaStream_t st) {
+void run_bn(GemmTcArgs& a, cudaStream_t st) {
   constexpr size_t STAGE = 128 * 128 + BN * 128;
   constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
   constexpr int MAXS = static_cast<int>((227 * 1024 - 2048 - STG) / STAGE);

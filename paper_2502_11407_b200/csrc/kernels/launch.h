@@ -37,6 +37,10 @@ struct GemmTcArgs {
   void* C = nullptr;
   int M = 0, N = 0, K = 0, batch = 1, BN = 128;
   int cs = 1;  // cluster size along N (A multicast), 1 = no cluster
+  int splits = 1;                         // split-K factor (fp32 output only)
+  float* partials = nullptr;              // (splits-1) partial tiles per output tile
+  unsigned long long* flags = nullptr;    // per-tile partner counters (zeroed at prepare)
+  unsigned long long flag_target = 0;     // counter value the owners wait for in the last launch
   int sms = 148;
   bool bf16 = false;
 };
