@@ -541,6 +541,66 @@ def run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, 
         pg.destroy_process_group()
 
 
+GRAPH_VS_TREE = {  # schedule-driven SIMT family: the construction decides the kernel's tiling
+    "gemm": {"kind": "gemm", "M": 1024, "K": 1024, "N": 1024},
+    "conv2d": {"kind": "conv2d", "I": [16, 64, 58, 58], "K": [64, 64, 3, 3], "S": 1},
+    "gemv": {"kind": "gemv", "M": 32768, "N": 4096},
+    "avgpool2d": {"kind": "avgpool2d", "I": [32, 256, 114, 114], "F": 3, "S": 1},
+}
+
+
+def run_graph_vs_tree(args, g, torch, hw, flush, device):
+    """SURVEY.md §8f rank 2 / the paper's core claim (graph construction >= tree construction,
+    PAPER.md:577): the same state-driven SIMT kernel family instantiated from the
+    graph-constructed schedule (optimize, B200 mode), from the on-device re-ranked top-k of the
+    graph, and from the Roller-style tree schedule (construct_tree, B200 mode), timed on B200."""
+    out = {}
+    for name, doc in GRAPH_VS_TREE.items():
+        op = g.TensorOpSpec.parse_text(json.dumps(doc))
+        gen = torch.Generator(device=device)
+        gen.manual_seed(0)
+        xs, o = make_inputs(op, {"op": doc}, gen, torch, device)
+        graph = g.optimize(op, hw, g.EngineConfig(seed=0, mode="b200", top_k=10))
+        tree = g.construct_tree(op, hw, 4, "b200")
+
+        def timed(sched, idx):
+            k = g.Kernel(op, sched, idx, "simt_f32")
+            for _ in range(2):
+                k.execute(xs, o)
+            ts = []
+            for _ in range(max(3, args.steps)):
+                flush.zero_()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                k.execute(xs, o)
+                e.record()
+                e.synchronize()
+                ts.append(s.elapsed_time(e))
+            return statistics.median(ts)
+
+        t_graph = timed(graph, 0)
+        rr = g.rerank(op, graph, xs, o, "simt_f32", iters=3)
+        t_rerank = timed(graph, rr["best"])
+        t_tree = timed(tree, 0)
+        unit_work = op.flops if doc["kind"] in ("gemm", "conv2d") else op.bytes
+        scale, unit = (1e12, "TFLOP/s") if doc["kind"] in ("gemm", "conv2d") else (1e9, "GB/s")
+        out[name] = {"unit": unit,
+                     "graph": {"ms": t_graph, "value": unit_work / (t_graph / 1e3) / scale,
+                               "schedule": graph[0]["state"]["repr"]},
+                     "graph_reranked": {"ms": t_rerank, "value": unit_work / (t_rerank / 1e3) / scale,
+                                        "schedule": graph[rr["best"]]["state"]["repr"], "index": rr["best"]},
+                     "tree": {"ms": t_tree, "value": unit_work / (t_tree / 1e3) / scale,
+                              "schedule": tree[0]["state"]["repr"]},
+                     "graph_over_tree": t_tree / t_graph}
+    geo = float(np.exp(np.mean([np.log(v["graph_over_tree"]) for v in out.values()])))
+    line = {"metric": "graph vs tree construction: measured B200 time of the SIMT family (speed-up)",
+            "value": geo, "unit": "x (geomean tree time / graph time)", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic U(-1,1)", "config": {"workload": "graph_vs_tree"},
+            "per_op": out}
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args):
     import torch
 
@@ -565,6 +625,13 @@ def run_ours(args):
         if pg:
             pg.barrier()
         torch.cuda.synchronize(device)
+
+    if args.workload == "graph_vs_tree":
+        if rank == 0:
+            run_graph_vs_tree(args, g, torch, hw, flush, device)
+        if pg:
+            pg.destroy_process_group()
+        return
 
     if args.workload == "suite":
         run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, local, pg, barrier)
@@ -675,7 +742,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(SEQUENCE_NAMES) + ["suite"], default="conv2d")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(SEQUENCE_NAMES) + ["suite", "graph_vs_tree"], default="conv2d")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -291,6 +291,7 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           int bn = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, bn_max));
           auto tiles = [&](int b) { return static_cast<int64_t>((g.M + 127) / 128) * ((g.N + b - 1) / b) * g.batch; };
           while (bn > 64 && tiles(bn) < sms) bn /= 2;
+          if (const char* e = std::getenv("GENSOR_GEMM_BN")) bn = std::atoi(e);  // developer override
           g.BN = bn;
           g.sms = sms;
           // A multicast across clusters of n-tiles (GENSOR_GEMM_CLUSTER=2|4): measured not to pay on
