@@ -56,11 +56,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // k-blocks: general mode (r, s, 32-channel chunk); packed mode (few channels, R*S*C <= 256): the
-  // whole window forms one K axis k = (r*S + s)*C + c, cut into 32-wide blocks (the ResNet stem:
-  // 147 taps -> 5 blocks instead of 49 channel-padded ones)
-  const int nck = packed ? (R * S * C + BK - 1) / BK : (C + BK - 1) / BK;
-  const int nk = packed ? nck : R * S * nck;
+  // k-blocks: general mode (r, s, 32-channel chunk); packed mode (few channels, C*S <= 64): per
+  // filter row r the (s, c) pairs form one K axis k = s*C + c, cut into 32-wide blocks
+  const int nck = packed ? (S * C + BK - 1) / BK : (C + BK - 1) / BK;
+  const int nk = packed ? R * nck : R * S * nck;
   const int64_t P = static_cast<int64_t>(N) * OH * OW;
   const int64_t plane = static_cast<int64_t>(H) * W;
 
@@ -105,12 +104,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
           for (int k = 0; k < BK; ++k)
             v[k] = (pv && ck * BK + k < C) ? __ldg(src + static_cast<int64_t>(k) * plane) : 0.0f;
         } else {
+          const int ck = kb % nck, r = kb / nck;
+          const float* src = base + static_cast<int64_t>(r) * W;
 #pragma unroll
           for (int k = 0; k < BK; ++k) {
-            const int kk = kb * BK + k;  // uniform across the warp
-            const int rs = kk / C, c = kk - rs * C, r = rs / S, sk = rs - r * S;
-            v[k] = (pv && rs < R * S) ? __ldg(base + static_cast<int64_t>(c) * plane + static_cast<int64_t>(r) * W + sk)
-                                      : 0.0f;
+            const int kk = ck * BK + k;  // uniform across the warp
+            const int sk = kk / C, c = kk - sk * C;
+            v[k] = (pv && sk < S) ? __ldg(src + static_cast<int64_t>(c) * plane + sk) : 0.0f;
           }
         }
       };
@@ -230,19 +230,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 // K[f][c][r][s] -> W'[r][s][f][c] (K-major B rows for the TMA); primary grid of the PDL pair.
 // Rows are padded to Cp = C rounded up to 4 channels (16 B, the TMA stride unit), pad = 0.
-// Packed mode (Cp = R*S*C rounded up to 4): W'[0][f][(r*S + s)*C + c].
+// Packed mode (Cp = S*C rounded up to 4): W'[r][f][s*C + c].
 __global__ void __launch_bounds__(256) k_filters_rsfc(const float* __restrict__ K, float* __restrict__ Wt, int F,
                                                       int C, int Cp, int RS, int S, int packed) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (packed) {
-    (void)S;
-    const int64_t tot = static_cast<int64_t>(F) * Cp;
+    const int R = RS / S;
+    const int64_t tot = static_cast<int64_t>(R) * F * Cp;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      const int kk = static_cast<int>(e % Cp);  // e = f*Cp + kk
-      const int f = static_cast<int>(e / Cp);
-      const int rs = kk / C, c = kk - rs * C;
-      Wt[e] = rs < RS ? __ldg(K + (static_cast<int64_t>(f) * C + c) * RS + rs) : 0.0f;
+      const int kk = static_cast<int>(e % Cp);  // e = (r*F + f)*Cp + kk
+      const int64_t rf = e / Cp;
+      const int f = static_cast<int>(rf % F), r = static_cast<int>(rf / F);
+      const int sk = kk / C, c = kk - sk * C;
+      Wt[e] = sk < S ? __ldg(K + ((static_cast<int64_t>(f) * C + c) * R + r) * S + sk) : 0.0f;
     }
     return;
   }
@@ -260,8 +261,8 @@ template <int BN>
 void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
   constexpr size_t STAGE = 128 * 128 + BN * 128;
   constexpr int STAGES = static_cast<int>((227 * 1024 - 2048 - 16384) / STAGE) >= 4 ? 4 : 3;
-  const int Cp = a.packed ? (a.R * a.S * a.C + 3) / 4 * 4 : (a.C + 3) / 4 * 4;
-  const int planes = a.packed ? 1 : a.R * a.S;
+  const int Cp = a.packed ? (a.S * a.C + 3) / 4 * 4 : (a.C + 3) / 4 * 4;
+  const int planes = a.packed ? a.R : a.R * a.S;
   if (!a.map_ready) {
     const uint64_t dw[3] = {static_cast<uint64_t>(Cp), static_cast<uint64_t>(a.F), static_cast<uint64_t>(planes)};
     const uint64_t sw[2] = {static_cast<uint64_t>(Cp) * 4, static_cast<uint64_t>(Cp) * a.F * 4};

@@ -371,9 +371,9 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           int bn = static_cast<int>(pow2_clamp(std::max<int64_t>(s.L ? s.tile(op, 1, 1) : 128, c.F), 64, 256));
           while (bn > 64 && bn / 2 >= c.F) bn /= 2;
           c.BN = bn;
-          c.packed = c.C * c.R * c.S <= 256 && c.C < 32;
-          const int Cp = c.packed ? (c.R * c.S * c.C + 3) / 4 * 4 : (c.C + 3) / 4 * 4;
-          const size_t planes = c.packed ? 1 : static_cast<size_t>(c.R) * c.S;
+          c.packed = c.C * c.S <= 64 && c.C < 32;
+          const int Cp = c.packed ? (c.S * c.C + 3) / 4 * 4 : (c.C + 3) / 4 * 4;
+          const size_t planes = c.packed ? c.R : static_cast<size_t>(c.R) * c.S;
           check_cuda(cudaMalloc(&k->ws, planes * c.F * Cp * 4), "conv_gemm workspace");
           c.ws_w = k->ws;
           const int64_t P = static_cast<int64_t>(c.N) * c.OH * c.OW;
