@@ -1,19 +1,19 @@
 // Tensor-core implicit-GEMM conv2d (stride 1), instantiated from a constructed conv2d schedule:
 //   O[n][f][h][w] = sum_{c,r,s} I[n][c][h+r][w+s] * K[f][c][r][s]   (op_spec.cpp:177-181)
-// GEMM view: M = output positions, N = f, K = (r, s, c). ONE launch, reference layouts in and out:
+// GEMM view: M = output positions, N = f, K = (r, s, c). Reference layouts in and out:
 //
+//   * launch 1 (pre-pass): NCHW -> NHWC copy of the input (2-row bands, DRAM-page friendly) and
+//     the K-major filter bank W'[r][s][f][c]; it triggers the conv grid early (programmatic
+//     dependent launch), whose producers / MMA warp wait for it with griddepcontrol.wait;
 //   * output tile = 8 rows x 2 images x 8 columns = 128 positions (one UMMA M), laid out in shared
 //     memory as row rho = h*16 + img*8 + w. A shift by filter row r is then rho + 16r (2 KB, a
 //     whole number of 1 KB swizzle atoms), so ONE staged box of (8+R-1) x 2 x 8 positions per
 //     (s, 128 B channel chunk) serves all R row shifts (3x fewer staged bytes for 3x3). The tile
 //     divides 56 x 56 exactly: C = [16,64,58,58] is 392 tiles, no idle lanes;
-//   * the A boxes are built by 8 producer warps straight from the NCHW input (software im2col:
-//     coalesced 32 B row runs, 16 B swizzled shared stores, fence.proxy.async) — no NHWC pre-pass
-//     and no extra HBM round trip;
-//   * the filter bank is converted to the K-major layout W'[r][s][f][c] by every CTA straight into
-//     shared memory at start (coalesced 16 B loads of K[f][c][r][s]), where it stays for the CTA's
-//     lifetime; each input row run is loaded once per channel chunk and shifted across lanes
-//     (shuffles) for the S filter columns;
+//   * 8 producer warps (two groups alternating channel chunks) move each 16 B channel chunk of
+//     the NHWC copy ONCE (LDG.128) and store it into every s-stage it feeds (conflict-free 16 B
+//     swizzled shared stores, fence.proxy.async); the filter bank is TMA-loaded into shared memory
+//     once and stays resident;
 //   * one thread issues tcgen05.mma (kind::tf32 or kind::f16) into two TMEM accumulators
 //     (double-buffered: the epilogue of tile i overlaps the MMAs of tile i+1);
 //   * 4 epilogue warps: tcgen05.ld -> streaming stores into NCHW.
