@@ -8,7 +8,9 @@
  *     reference's ErrorCode enum (include/gensor/error.hpp:8-27) as ordinal + 1;
  *   - gensor_last_error() returns a thread-local "<CodeName>: detail" message, the reference's
  *     what() text (error.hpp:33-34);
- *   - handles are opaque and immutable after creation, safe to share across threads;
+ *   - op / hw / schedule handles are opaque and immutable after creation, safe to share across
+ *     threads; a kernel handle runs one execute at a time (per-handle device workspace), so use
+ *     one kernel handle per concurrent stream;
  *   - lifetimes: an op must outlive every schedule and kernel made from it (the reference's
  *     ETIRState keeps a non-owning op pointer, etir.hpp:75); a hw must outlive schedules;
  *   - JSON outputs use caller buffers: on cap < need the call returns GENSOR_ETRUNCATED and
