@@ -450,17 +450,22 @@ __device__ __forceinline__ void issue_band(const StreamWinArgs& a, const float* 
 // oracle_interpret): Markstein's sequence q0 = acc*y, r = acc - F^2*q0 (exact by FMA),
 // q = q0 + r*y with y = RN(1/F^2) is correctly rounded for normal results (checked against exact
 // rational division for F^2 in {9, 25, 49}); tiny / non-finite sums take the IEEE division.
+__device__ __noinline__ float div_window_slow(float acc, float d) { return __fdiv_rn(acc, d); }
+
 __device__ __forceinline__ float div_window(float acc, float d, float y) {
   const float q0 = acc * y;
   const float r = fmaf(-q0, d, acc);
-  const float q = fmaf(r, y, q0);
-  return (fabsf(acc) > 1e-30f && fabsf(acc) < 1e30f) ? q : __fdiv_rn(acc, d);
+  float q = fmaf(r, y, q0);
+  // Out-of-line IEEE division only where the Markstein step could over/underflow; keeping it a
+  // real (not if-converted) branch leaves 3 FMA-pipe ops per output on the hot path.
+  if (__builtin_expect(!(fabsf(acc) > 1e-30f && fabsf(acc) < 1e30f), 0)) q = div_window_slow(acc, d);
+  return q;
 }
 
 template <bool DW>
 __device__ __forceinline__ void store_row(const StreamWinArgs& a, float* orow, int ox, const float (&acc)[kTW]) {
   float o[kTW];
-  const float d = static_cast<float>(a.divisor), y = 1.0f / d;
+  const float d = static_cast<float>(a.divisor), y = __frcp_rn(d);
 #pragma unroll
   for (int j = 0; j < kTW; ++j) o[j] = DW ? acc[j] : div_window(acc[j], d, y);
   if constexpr (kTW == 2) {
@@ -693,7 +698,7 @@ __global__ void __launch_bounds__(kGlobalPlanes) k_window_global(const StreamWin
                                                                  float* __restrict__ out) {
   extern __shared__ float pl[];
   const int hw = static_cast<int>(a.H * a.W);
-  const float dv = static_cast<float>(a.divisor), y = 1.0f / dv;
+  const float dv = static_cast<float>(a.divisor), y = __frcp_rn(dv);
   for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * kGlobalPlanes; g0 < a.planes;
        g0 += static_cast<int64_t>(gridDim.x) * kGlobalPlanes) {
     const int np = static_cast<int>(min(static_cast<int64_t>(kGlobalPlanes), a.planes - g0));
