@@ -127,6 +127,19 @@ int gensor_schedule_from_trace(const gensor_op* op, const gensor_hw* hw, const c
                                int mode, gensor_schedule** out);
 /* {state:{level,tiles,vthreads,repr}, trace, cost, seed, iterations}; index -1 = all results. */
 int gensor_schedule_json(const gensor_schedule* s, int index, char* buf, size_t cap, size_t* need);
+/* Explicit construction-chain analysis (the reference's markov-verify module, markov.hpp:1-70,
+ * SPEC.md:380-457): enumerates the schedule space reachable under the candidate policy frozen at
+ * an annealing iteration and reports per-level SCCs / irreducibility / stationary entropy,
+ * aperiodicity, the value iteration of Eqs. 5-6 and its greedy policy path as JSON.
+ * caps_json (optional) keys: max_states (50000), fixed_iteration (10), enable_inv_tile (true),
+ * vthread_options ([1,2,4,8]), max_tile_factor (2), mode ("reference"|"b200"), detail (false:
+ * every state, edge, value and stationary vector). GENSOR_ESPACE_TOO_LARGE past max_states. */
+int gensor_analyze(const gensor_op* op, const gensor_hw* hw, const char* caps_json, char* buf, size_t cap,
+                   size_t* need);
+/* Portable C source of result `index`'s tiled loop nest (the SPEC's emit_source, SPEC.md:488-496;
+ * absent from the reference): deterministic text, guards iff padding, double accumulation.
+ * GENSOR_EINCOMPLETE_STATE for an incomplete state (e.g. gensor_construct snapshots). */
+int gensor_emit_source(const gensor_schedule* s, int index, char* buf, size_t cap, size_t* need);
 int gensor_schedule_count(const gensor_schedule* s);
 void gensor_schedule_free(gensor_schedule* s);
 

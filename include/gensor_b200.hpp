@@ -140,6 +140,10 @@ class Schedules {
   std::string json(int index) const {
     return json_out([&](char* b, size_t c, size_t* n) { return gensor_schedule_json(h_, index, b, c, n); });
   }
+  // Portable C source of result `index`'s loop nest (SPEC.md:488-496 emit_source).
+  std::string emit_source(int index) const {
+    return json_out([&](char* b, size_t c, size_t* n) { return gensor_emit_source(h_, index, b, c, n); });
+  }
   const gensor_schedule* handle() const { return h_; }
 
  private:

@@ -31,6 +31,8 @@ def lib() -> ctypes.CDLL:
             fn.argtypes = [ctypes.c_char_p] * n
         L.ref_candidates.restype = ctypes.c_void_p
         L.ref_candidates.argtypes = [ctypes.c_char_p] * 4 + [ctypes.c_int, ctypes.c_double]
+        L.ref_analyze.restype = ctypes.c_void_p
+        L.ref_analyze.argtypes = [ctypes.c_char_p] * 3
         L.ref_tree.restype = ctypes.c_void_p
         L.ref_tree.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int]
         L.ref_free.argtypes = [ctypes.c_void_p]
@@ -74,6 +76,10 @@ def state_eval(op, hw, trace) -> dict:
 
 def candidates(op, hw, trace, cfg=None, iteration=0, temperature=1.0) -> dict:
     return _call(lib().ref_candidates, _t(op), _t(hw), _t(trace), _t(cfg or {}), iteration, temperature)
+
+
+def analyze(op, hw, caps=None) -> dict:
+    return _call(lib().ref_analyze, _t(op), _t(hw), _t(caps or {}))
 
 
 def tree(op, hw, beam=4) -> dict:

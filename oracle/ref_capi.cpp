@@ -8,6 +8,7 @@
 //   enumerate_candidates            engine.hpp:54-57
 //   memory_traffic / traffic_oracle / estimate_cost   cost_model.hpp:32-71
 //   construct_tree / greedy_fit_step                  tree_baseline.hpp:21-26
+//   enumerate_space / check_* / stationary / value    markov.hpp:40-67
 // Every entry point takes JSON text and returns a malloc'd JSON string (free with ref_free).
 // Nothing in the product (paper_2502_11407_b200/) links or loads this file.
 #include <chrono>
@@ -20,6 +21,7 @@
 #include "gensor/error.hpp"
 #include "gensor/etir.hpp"
 #include "gensor/hardware.hpp"
+#include "gensor/markov.hpp"
 #include "gensor/op_spec.hpp"
 #include "gensor/tree_baseline.hpp"
 
@@ -271,6 +273,54 @@ char* ref_op_info(const char* op_text) {
     out["dtype_bytes"] = op.dtype_bytes();
     out["label"] = op.label();
     out["json"] = op.to_json();
+    return dup(out.dump());
+  } catch (const std::exception& e) {
+    return dup(err_json(e).dump());
+  }
+}
+
+// The reference's chain model and analyses (markov.cpp:40-364), per state in its own discovery
+// order: repr, level, complete, absorbing, terminal, rows; per-level irreducibility; aperiodicity;
+// value iteration; the stationary vector of every level listed in caps["stationary_levels"].
+char* ref_analyze(const char* op_text, const char* hw_text, const char* caps_text) {
+  try {
+    TensorOpSpec op = TensorOpSpec::parse_text(op_text);
+    HardwareSpec hw = HardwareSpec::load_text(hw_text);
+    Json c = Json::parse(caps_text);
+    ChainCaps caps;
+    if (c.contains("max_states")) caps.max_states = c["max_states"].get<int>();
+    if (c.contains("fixed_iteration")) caps.fixed_iteration = c["fixed_iteration"].get<int>();
+    if (c.contains("enable_inv_tile")) caps.enable_inv_tile = c["enable_inv_tile"].get<bool>();
+    if (c.contains("vthread_options")) caps.vthread_options = c["vthread_options"].get<std::vector<int64_t>>();
+    if (c.contains("max_tile_factor")) caps.max_tile_factor = c["max_tile_factor"].get<int64_t>();
+    ChainModel m = enumerate_space(op, hw, caps);
+    Json out;
+    Json states = Json::array(), rows = Json::array();
+    for (int i = 0; i < m.num_states(); ++i) {
+      states.push_back(m.states[static_cast<size_t>(i)].repr());
+      Json row = Json::array();
+      for (const ChainEdge& e : m.rows[static_cast<size_t>(i)])
+        row.push_back(Json::array({e.to, e.prob, action_json(e.action), e.artificial ? 1 : 0}));
+      rows.push_back(row);
+    }
+    out["states"] = states;
+    out["rows"] = rows;
+    out["level"] = m.level_of;
+    out["complete"] = m.complete;
+    out["absorbing"] = m.absorbing;
+    out["terminal"] = m.terminal_value;
+    out["irreducible"] = check_irreducible_per_level(m);
+    out["aperiodic"] = check_aperiodic(m);
+    ValueTable vt = value_iteration(m);
+    out["value"] = vt.value;
+    out["iterations"] = vt.iterations;
+    Json pol = Json::array();
+    for (const auto& p : vt.policy) pol.push_back(p ? action_json(*p) : Json());
+    out["policy"] = pol;
+    Json st = Json::object();
+    if (c.contains("stationary_levels"))
+      for (int l : c["stationary_levels"].get<std::vector<int>>()) st[std::to_string(l)] = stationary_distribution(m, l);
+    out["stationary"] = st;
     return dup(out.dump());
   } catch (const std::exception& e) {
     return dup(err_json(e).dump());

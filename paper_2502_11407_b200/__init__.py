@@ -10,6 +10,7 @@ from .gensor import (  # noqa: F401
     Kernel,
     Schedules,
     TensorOpSpec,
+    analyze,
     anneal_cache_multiplier,
     caching_benefit,
     construct,

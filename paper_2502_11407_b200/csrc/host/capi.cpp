@@ -12,6 +12,8 @@
 
 #include "cost.hpp"
 #include "device.hpp"
+#include "emit.hpp"
+#include "markov.hpp"
 #include "engine.hpp"
 #include "error.hpp"
 #include "hw.hpp"
@@ -310,6 +312,42 @@ int gensor_schedule_json(const gensor_schedule* s, int index, char* buf, size_t 
     std::string all = "[";
     for (size_t i = 0; i < s->results.size(); ++i) all += (i ? "," : "") + result_json(s, s->results[i]);
     return emit(all + "]", buf, cap, need);
+  });
+}
+
+int gensor_emit_source(const gensor_schedule* s, int index, char* buf, size_t cap, size_t* need) {
+  if (!s) return fail(GENSOR_EINVALID, "null schedule");
+  return guarded([&]() -> int {
+    if (index < 0 || index >= static_cast<int>(s->results.size()))
+      return fail(GENSOR_EINVALID, "schedule index out of range");
+    const gb::Result& r = s->results[static_cast<size_t>(index)];
+    if (!r.state.complete()) throw gb::Error(gb::Code::IncompleteState, "emit_source needs a complete state");
+    return emit(gb::emit_source(*s->op, r.state, trace_json(r.trace)), buf, cap, need);
+  });
+}
+
+int gensor_analyze(const gensor_op* op, const gensor_hw* hw, const char* caps_json, char* buf, size_t cap,
+                   size_t* need) {
+  if (!op || !hw) return fail(GENSOR_EINVALID, "null argument");
+  return guarded([&]() -> int {
+    gb::ChainCaps caps;
+    bool detail = false;
+    if (caps_json && *caps_json) {
+      const gb::json::Value c = gb::json::parse(caps_json);
+      if (!c.is_object()) throw gb::Error(gb::Code::ConfigError, "caps must be a JSON object");
+      if (const auto* v = c.find("max_states")) caps.max_states = static_cast<int>(v->as_int());
+      if (const auto* v = c.find("fixed_iteration")) caps.fixed_iteration = static_cast<int>(v->as_int());
+      if (const auto* v = c.find("enable_inv_tile")) caps.enable_inv_tile = v->as_int() != 0;
+      if (const auto* v = c.find("max_tile_factor")) caps.max_tile_factor = v->as_int();
+      if (const auto* v = c.find("vthread_options")) {
+        caps.vthread_options.clear();
+        for (const auto& x : v->arr) caps.vthread_options.push_back(x.as_int());
+      }
+      if (const auto* v = c.find("mode")) caps.mode = v->as_string() == "b200" ? gb::Mode::B200 : gb::Mode::ReferenceCompat;
+      if (const auto* v = c.find("detail")) detail = v->as_int() != 0;
+    }
+    if (caps.max_states < 1) throw gb::Error(gb::Code::ConfigError, "max_states must be >= 1");
+    return emit(gb::analysis_json(op->op, hw->hw, caps, detail), buf, cap, need);
   });
 }
 

@@ -91,6 +91,7 @@ bool candidates(const OpDesc& op, const HwModel& hw, const Sched& s, const Engin
   if (!s.complete()) {
     const int level = s.edit_level();
     for (ActKind kind : {ActKind::Tile, ActKind::InvTile}) {
+      if (kind == ActKind::InvTile && !cfg.enable_inv_tile) continue;
       for (int a = 0; a < op.naxes; ++a) {
         for (int64_t f = 2; f <= cfg.max_tile_factor; f *= 2) {
           const Action act{kind, a, f};

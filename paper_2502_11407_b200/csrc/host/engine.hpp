@@ -36,6 +36,7 @@ struct EngineCfg {
   int64_t max_tile_factor = 2;
   Mode mode = Mode::ReferenceCompat;
   int threads = 0;  // 0 = min(restarts, hardware threads)
+  bool enable_inv_tile = true;  // ActionSpace::enable_inv_tile (engine.hpp:31): chain analysis only
   void validate() const;  // throws ConfigError (engine.cpp:11-22)
 };
 

@@ -101,6 +101,8 @@ def _load() -> ctypes.CDLL:
         "gensor_kernel_set_timing": (I, [P, I]),
         "gensor_kernel_timings": (I, [P, ctypes.POINTER(ctypes.c_float), I, IP, ctypes.c_char_p, SZ]),
         "gensor_rerank": (I, [P, P, I, PP, I, P, P, I, ctypes.c_char_p, SZ, SZP]),
+        "gensor_emit_source": (I, [P, I, ctypes.c_char_p, SZ, SZP]),
+        "gensor_analyze": (I, [P, P, S, ctypes.c_char_p, SZ, SZP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -119,7 +121,7 @@ EXPORTED = [
     "gensor_anneal_cache_multiplier", "gensor_record_probability", "gensor_derive_seed",
     "gensor_kernel_prepare", "gensor_kernel_info", "gensor_execute", "gensor_execute_host",
     "gensor_kernel_free", "gensor_launch_count", "gensor_kernel_set_timing", "gensor_kernel_timings",
-    "gensor_rerank",
+    "gensor_rerank", "gensor_emit_source", "gensor_analyze",
 ]
 
 
@@ -132,7 +134,7 @@ def _check(status: int) -> None:
         raise GensorError(status, _lib.gensor_last_error().decode())
 
 
-def _json_call(fn, *args) -> Any:
+def _text_call(fn, *args) -> str:
     need = ctypes.c_size_t(0)
     buf = ctypes.create_string_buffer(1 << 16)
     st = fn(*args, buf, len(buf), ctypes.byref(need))
@@ -140,7 +142,11 @@ def _json_call(fn, *args) -> Any:
         buf = ctypes.create_string_buffer(need.value)
         st = fn(*args, buf, len(buf), ctypes.byref(need))
     _check(st)
-    return json.loads(buf.value.decode())
+    return buf.value.decode()
+
+
+def _json_call(fn, *args) -> Any:
+    return json.loads(_text_call(fn, *args))
 
 
 def _text(doc: Any) -> bytes:
@@ -278,6 +284,10 @@ class Schedules:
     def __len__(self):
         return len(self.results)
 
+    def emit_source(self, index: int = 0) -> str:
+        """Portable C source of result `index`'s loop nest (SPEC.md:488-496 emit_source)."""
+        return _text_call(_lib.gensor_emit_source, self._h, index)
+
     def __getitem__(self, i):
         return self.results[i]
 
@@ -334,6 +344,11 @@ def enumerate_candidates(op: TensorOpSpec, hw: HardwareSpec, trace, cfg: EngineC
     cfg = cfg or EngineConfig()
     c = cfg._struct()
     return _json_call(_lib.gensor_candidates, op._h, hw._h, _text(trace), ctypes.byref(c), iteration)["candidates"]
+
+
+def analyze(op: TensorOpSpec, hw: HardwareSpec, caps: dict | None = None) -> dict:
+    """Construction-chain analysis (markov.hpp / SPEC.md:380-457 markov-verify), see gensor_analyze."""
+    return _json_call(_lib.gensor_analyze, op._h, hw._h, _text(caps or {}))
 
 
 def caching_benefit(lat_low, bw_low, lat_high, bw_high, s_bytes) -> float:

@@ -2,7 +2,7 @@
 unmodified reference construct library compiled by oracle/Makefile). Run here, where
 /root/reference exists; the fixtures are committed so the CPU tests pin parity on any box.
 
-  python tools/make_golden.py
+  python tools/make_golden.py [--markov-only]
 """
 import json
 import os
@@ -26,9 +26,37 @@ EXTRA_OPS = {
 }
 
 
+# Chain-analysis cases (markov.cpp): small enumerable spaces, incl. a 2-level (L=1) profile.
+TWO_LEVEL = dict(PROFILES["generic"], name="generic-2level", levels=PROFILES["generic"]["levels"][:2])
+MARKOV_CASES = [
+    ("generic", {"kind": "gemv", "M": 4, "N": 2}, {}),
+    ("generic", {"kind": "gemv", "M": 4, "N": 2}, {"enable_inv_tile": False, "stationary_levels": []}),
+    ("two_level", {"kind": "gemm", "M": 4, "K": 4, "N": 4}, {}),
+    ("two_level", {"kind": "gemv", "M": 16, "N": 8}, {"fixed_iteration": 0}),
+    ("b200_ref", {"kind": "avgpool2d", "I": [1, 1, 5, 5], "F": 2, "S": 1}, {"vthread_options": [1, 2]}),
+]
+
+
+def markov():
+    profiles = dict(PROFILES, two_level=TWO_LEVEL)
+    out = {"generator": "tools/make_golden.py over oracle/_ref markov.cpp (reference, unmodified)",
+           "profiles": profiles, "cases": []}
+    for pname, op, caps in MARKOV_CASES:
+        r = ref.analyze(op, profiles[pname], dict({"stationary_levels": [0]}, **caps))
+        assert "error" not in r, r
+        out["cases"].append({"profile": pname, "op": op, "caps": caps, "ref": r})
+    path = os.path.join(ROOT, "tests", "golden", "markov_golden.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(path, os.path.getsize(path), "bytes")
+
+
 def main():
     if not ref.available():
         sys.exit("oracle/_ref not built: make -C oracle ref")
+    markov()
+    if "--markov-only" in sys.argv:
+        return
     ops = dict(CONFIG_OPS)
     ops.update(EXTRA_OPS)
     out = {"generator": "tools/make_golden.py over oracle/_ref (reference proj/src, unmodified)",
