@@ -10,10 +10,11 @@
 //     whole number of 1 KB swizzle atoms), so ONE staged box of (8+R-1) x 2 x 8 positions per
 //     (s, 128 B channel chunk) serves all R row shifts (3x fewer staged bytes for 3x3). The tile
 //     divides 56 x 56 exactly: C = [16,64,58,58] is 392 tiles, no idle lanes;
-//   * 8 producer warps (two groups alternating channel chunks) move each 16 B channel chunk of
-//     the NHWC copy ONCE (LDG.128) and store it into every s-stage it feeds (conflict-free 16 B
-//     swizzled shared stores, fence.proxy.async); the filter bank is TMA-loaded into shared memory
-//     once and stays resident;
+//   * one producer thread TMA-loads each (s, channel chunk) box straight into its stage: the NHWC
+//     copy is described by a 4-D tensor map whose dimensions are permuted to (c, w, n, h), so a
+//     box {chunk, 8, 2, 8+R-1} lands as rows rho = h*16 + img*8 + w, 128 B swizzled — the layout
+//     the MMA descriptors expect, no software producers; the filter bank is TMA-loaded into
+//     shared memory once and stays resident;
 //   * one thread issues tcgen05.mma (kind::tf32 or kind::f16) into two TMEM accumulators
 //     (double-buffered: the epilogue of tile i overlaps the MMAs of tile i+1);
 //   * 4 epilogue warps: tcgen05.ld -> streaming stores into NCHW.
@@ -37,9 +38,8 @@ using namespace tc;
 constexpr int kTH = 8;       // output rows per tile
 constexpr int kTI = 2;       // images per tile
 constexpr int kTW = 8;       // output columns per tile
-constexpr int kProducerWarps = 8;  // two groups of 4 warps, each group fills every other stage
-constexpr int kGroupThreads = 128;
-constexpr int kThreads = 32 * (kProducerWarps + 1 + 4);  // producers, MMA, 4 epilogue warps
+constexpr int kProducerWarps = 1;  // one elected thread issues the A-box TMA loads
+constexpr int kThreads = 32 * (kProducerWarps + 1 + 4);  // producer, MMA, 4 epilogue warps
 
 template <typename T>
 struct ConvTraits;
@@ -54,14 +54,9 @@ struct ConvTraits<__nv_bfloat16> {
   static constexpr bool kF16 = true;
 };
 
-__device__ __forceinline__ void st_shared_v4(void* p, uint4 v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-
 template <typename T, int FN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_conv_tc(const T* __restrict__ X, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
+    k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
               int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
               long long* __restrict__ trace) {
   // developer trace (GENSOR_CONV_TRACE=<file>): clock64 marks per CTA, 64 slots
@@ -94,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], kGroupThreads);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(wbar, 1);
@@ -111,108 +106,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kProducerWarps) {
-    // ---- producers: A box rows rho = hh*16 + img*8 + w (128 B of channels) from the NHWC copy.
-    // One PASS = the S stages (s = 0..S-1) of one 128 B channel chunk: each (hh, img, column)
-    // 16 B chunk of X is loaded ONCE (LDG.128, 8 lanes per 128 B position row) and stored into
-    // every s-stage whose tile column it feeds (column x feeds w = x - s).
-    // Group g (warps 4g..4g+3) takes passes p = g (mod 2).
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
-    const int grp = warp >> 2, pw = warp & 3;
-    const int q = lane & 7, sub = lane >> 3;  // 16 B chunk within the 128 B row, row slot 0..3
-    const int cols = kTW + S - 1;              // input columns per tile row
-    const int rows = (kTH + R - 1) * kTI;      // (hh, img) rows per pass
-    const int nrow_items = rows * cols;        // position rows to move per pass
-    int it = 0, pass = 0, pstage = 0;
-    long long pwait = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int np = t / tiles_img;
-      const int h0 = ((t % tiles_img) / tiles_w) * kTH;
-      const int w0 = (t % tiles_w) * kTW;
-      for (int ck = 0; ck < nck; ++ck, ++pass, it += S) {
-        if ((pass & 1) != grp) continue;
-        // 4 position rows per warp instruction (8 lanes x 16 B each); a group moves 16 per step
-        auto load_row = [&](int ri) -> uint4 {
-          const int x = ri % cols, rr = ri / cols;  // input column, (hh, img) row
-          const int img = rr & 1, hh = rr >> 1;
-          const int n = np * kTI + img, hi = h0 + hh, wi = w0 + x;
-          const bool ok = ri < nrow_items && n < N && hi < H && wi < W &&
-                          (ck * CK + q * static_cast<int>(16 / sizeof(T))) < C;
-          const uint4* src =
-              reinterpret_cast<const uint4*>(X + (((static_cast<int64_t>(n) * H + hi) * W + wi) * C + ck * CK)) + q;
-          return ok ? __ldg(src) : make_uint4(0u, 0u, 0u, 0u);
-        };
-        auto store_row = [&](int ri, int s, uint4 v) {
-          const int x = ri % cols, rr = ri / cols;
-          const int w = x - s;
-          if (ri >= nrow_items || w < 0 || w >= kTW) return;
-          const int img = rr & 1, hh = rr >> 1;
-          const int rho = hh * (kTI * kTW) + img * kTW + w;
-          st_shared_v4(asm_ + ((it + s) % STAGES) * a_bytes + rho * 128 + ((q ^ (rho & 7)) << 4), v);
-        };
-        const int first = pw * 4 + sub;
-        if (R == 3 && S == 3) {
-          // 3x3 fast path: a warp owns 5 of the 20 (hh, img) rows; lane = (16 B chunk q, column
-          // slot xr) loads columns x = xr, xr + 4, xr + 8 (< 10) of each row, every offset
-          // incremental; stage s receives column x at tile column w = x - s (swizzle q ^ w)
-          constexpr int kRows = 5, kJ = 3;
-          const int xr = sub;
-          uint4 v[kRows][kJ];
-#pragma unroll
-          for (int i = 0; i < kRows; ++i) {
-            const int rr = pw * kRows + i, img = rr & 1, hh = rr >> 1;
-            const int n = np * kTI + img, hi = h0 + hh;
-            const bool row_ok = n < N && hi < H && (ck * CK + q * static_cast<int>(16 / sizeof(T))) < C;
-            const T* rowp = X + ((static_cast<int64_t>(n) * H + hi) * W + w0) * C + ck * CK;
-#pragma unroll
-            for (int j = 0; j < kJ; ++j) {
-              const int x = xr + 4 * j;
-              v[i][j] = (row_ok && x < 10 && w0 + x < W)
-                            ? __ldg(reinterpret_cast<const uint4*>(rowp + static_cast<int64_t>(x) * C) + q)
-                            : make_uint4(0u, 0u, 0u, 0u);
-            }
-          }
-#pragma unroll
-          for (int s = 0; s < 3; ++s) {
-            const int k = it + s;
+    // ---- producer: one TMA box per (tile, channel chunk, s): rows rho = hh*16 + img*8 + w of
+    // input positions (n0 + img, h0 + hh, w0 + s + w), 128 B of channels each; out-of-range
+    // positions / channels are zero-filled by the TMA unit.
+    if (elect_one()) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
+      tma_prefetch(&mapX);
+      long long pwait = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int n0 = (t / tiles_img) * kTI;
+        const int h0 = ((t % tiles_img) / tiles_w) * kTH;
+        const int w0 = (t % tiles_w) * kTW;
+        for (int ck = 0; ck < nck; ++ck)
+          for (int s = 0; s < S; ++s, ++it) {
+            const int st = it % STAGES;
             const long long tw0 = trace ? clock64() : 0;
-            mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
+            mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
             if (trace) pwait += clock64() - tw0;
-            uint8_t* box = asm_ + (k % STAGES) * a_bytes;
-#pragma unroll
-            for (int i = 0; i < kRows; ++i) {
-              const int rr = pw * kRows + i;
-#pragma unroll
-              for (int j = 0; j < kJ; ++j) {
-                const int w = xr + 4 * j - s;
-                if (w >= 0 && w < kTW) st_shared_v4(box + (rr * 8 + w) * 128 + ((q ^ w) << 4), v[i][j]);
-              }
-            }
-            fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
-            mbar_arrive(&full[k % STAGES]);
+            mbar_arrive_expect_tx(&full[st], a_bytes);
+            tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * CK, w0 + s, n0, h0);
           }
-        } else {
-          const long long tw0 = trace ? clock64() : 0;
-          for (int s = 0; s < S; ++s) {
-            const int k = it + s;
-            mbar_wait(&empty[k % STAGES], ((k / STAGES) & 1) ^ 1);
-          }
-          if (trace) pwait += clock64() - tw0;
-          for (int base = first; base < nrow_items; base += 16 * 8) {
-            uint4 v[8];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) v[b] = load_row(base + 16 * b);
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-              for (int s = 0; s < S; ++s) store_row(base + 16 * b, s, v[b]);
-          }
-          fence_proxy_async_smem();
-          for (int s = 0; s < S; ++s) mbar_arrive(&full[(it + s) % STAGES]);
-        }
-        if (warp == 0 && lane == 0 && pstage < 20) CONV_TRACE(20 + pstage, clock64());
-        ++pstage;
       }
+      CONV_TRACE(61, pwait);
     }
-    if (warp == 0 && lane == 0) CONV_TRACE(61, pwait);
   } else if (warp == kMmaWarp) {
     if (elect_one()) {
       CONV_TRACE(0, clock64());
@@ -415,6 +332,13 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.C) * a.F * es};
     const uint32_t bw[3] = {static_cast<uint32_t>(CK), static_cast<uint32_t>(FN), 1};
     encode_map(&a.mapW, es == 2, es == 4, a.ws_w, 3, dw, sw, bw);
+    // NHWC copy viewed as (c, w, n, h): box {CK, 8, 2, 8+R-1} -> smem rows h*16 + img*8 + w
+    const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.N),
+                            static_cast<uint64_t>(a.H)};
+    const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.H) * a.W * a.C * es,
+                            static_cast<uint64_t>(a.W) * a.C * es};
+    const uint32_t bx[4] = {static_cast<uint32_t>(CK), kTW, kTI, static_cast<uint32_t>(kTH + a.R - 1)};
+    encode_map(&a.mapX, es == 2, es == 4, a.ws_x, 4, dx, sx, bx);
     a.maps_ready = true;
   }
   auto launch = [&](auto kern) {
@@ -446,7 +370,7 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a.ws_x), a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
                                   tiles_w, total, trace),
                "conv_tc launch");
     if (trace) {  // developer path: synchronous dump of the last launch

@@ -322,7 +322,9 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
              << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true"
              << ",\"cluster_n\":" << g.cs << ",\"split_k\":" << g.splits << "}";
-        } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16)) {
+        } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16) &&
+                   !(std::getenv("GENSOR_CONV_FAMILY") && std::string(std::getenv("GENSOR_CONV_FAMILY")) == "gemm" &&
+                     !bf16)) {  // developer override: A/B the two conv families on one shape
           k->family = Family::ConvTc;
           k->launches = 1;
           k->launch_names = {"conv_tc"};

@@ -50,6 +50,7 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
 // ---- tensor-core implicit-GEMM conv2d family (conv_tc.cu) ----
 struct ConvTcArgs {
   CUtensorMap mapW;   // over the W'[r][s][f][c] workspace, built once
+  CUtensorMap mapX;   // over the NHWC copy, dimensions permuted to (c, w, n, h)
   bool maps_ready = false;
   void* ws_w = nullptr;  // W' workspace, rewritten by the pre-pass launch of every execute
   void* ws_x = nullptr;  // NHWC copy of the input, rewritten by the pre-pass launch

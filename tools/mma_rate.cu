@@ -66,6 +66,49 @@ __global__ void k_rate(long long* out, int iters) {
   }
 }
 
+
+// The conv_tc issue pattern: 4 rotating 20 KB A stages, each feeding 3 filter-row shifts (+2 KB)
+// x 4 k-steps against a resident 72 KB B bank (distinct operands every MMA).
+template <int N>
+__global__ void k_rate_conv(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  constexpr uint32_t IDESC = instr_desc(2, 128, N, 0, 0);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<256>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 32) {
+    const uint32_t a = smem_u32(smem), b = a + 4 * 20480;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t as = a + (i & 3) * 20480;
+      const uint32_t bs = b + (i % 6) * (3 * N * 128 / 2 > 12288 ? 0 : 0);
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_tf32(tmem, smem_desc_sw128(as + r * 2048 + k * 32, 16, 1024),
+                   smem_desc_sw128(bs + (r * 6 + (i % 6)) * (N * 128) % (9 * N * 128) + k * 32, 16, 1024), IDESC, 1u);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 // Round trip of `k` MMAs + tcgen05.commit -> mbarrier wait, repeated.
 __global__ void k_commit_rtt(long long* out, int k, int reps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -153,6 +196,18 @@ int main() {
   rate<false, 128, true>(d, sms, "tf32 B MN-major");
   rate<true, 64, true>(d, sms, "bf16 B MN-major");
   rate<true, 256, true>(d, sms, "bf16 B MN-major");
+  {
+    const int iters = 256;
+    const int smem = 4 * 20480 + 9 * 64 * 128;
+    CK(cudaFuncSetAttribute(k_rate_conv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_rate_conv<64><<<sms, 64, smem>>>(d, iters);
+    CK(cudaDeviceSynchronize());
+    long long h[256];
+    CK(cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost));
+    double avg = 0;
+    for (int i = 0; i < sms; ++i) avg += h[i];
+    printf("tf32 N=64 conv pattern (distinct operands): %.1f cycles/MMA\n", avg / sms / (iters * 12.0));
+  }
   for (int k : {0, 1, 4, 12}) {
     CK(cudaFuncSetAttribute(k_commit_rtt, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     k_commit_rtt<<<sms, 64, 65536>>>(d, k, 64);
