@@ -397,6 +397,272 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// conv_ns: stride-1 tf32 conv with S*F <= 256, reading the NCHW input IN PLACE (no NHWC copy).
+//   * tile = 4 output rows x 32 columns of one image; the A operand is MN-major (32 consecutive
+//     input columns of one row = one 128 B row per channel, 32 B-atom swizzle), staged per
+//     32-channel chunk as (4 + R - 1) row chunks of 4 KB: a filter-row shift r is +4 KB;
+//   * the filter columns s are folded into N: B = W'[r][chunk][s][f][c] rows (s, f), so one
+//     N = S*FN MMA computes, for every staged input position, its products with all S filter
+//     columns (full tensor-core rate at N = 192 instead of N = 64 per s, and no s-shifted
+//     copies of A); the epilogue adds column s of TMEM lane w + s into output w with a warp
+//     shuffle: outputs w < 32 - (S - 1) of each tile are valid;
+//   * 8 software producer warps (two groups alternating chunks) load 128 B input row segments
+//     with coalesced LDG and store them swizzled (the input rows are only 8 B aligned, which
+//     TMA cannot address); the filter bank is TMA-loaded once and stays resident.
+constexpr int kNsRows = 4, kNsCols = 32;
+constexpr int kNsEpi = 4;  // epilogue warps, one per TMEM lane quarter
+constexpr int kNsThreads = 32 * (1 + 1 + kNsEpi);
+
+template <int STAGES>
+__global__ void __launch_bounds__(kNsThreads, 1)
+    k_conv_ns(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
+              int C, int H, int W, int F, int FN, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
+              int valid_w, long long* __restrict__ trace) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nck = (C + 31) / 32;
+  const int rows = kNsRows + R - 1;
+  const int ncol = S * FN;  // UMMA N
+  const uint32_t w_bytes = static_cast<uint32_t>(R * nck * ncol) * 128;
+  const uint32_t a_bytes = static_cast<uint32_t>(rows) * 4096;
+  uint8_t* wsm = smem;
+  uint8_t* asm_ = smem + w_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + STAGES * a_bytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* wbar = empty + STAGES;
+  uint64_t* acc_full = wbar + 1;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_img = tiles_h * tiles_w;
+#define NS_TRACE(slot, v) \
+  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
+  constexpr int kMma = 1;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(wbar, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kNsEpi);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMma) {
+    if (2 * ncol > 256) tmem_alloc<512>(tmem_slot);
+    else tmem_alloc<256>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- producer: one TMA box per (tile, 32-channel chunk) from the NHWC copy viewed as
+    // (c, w, h, n): box {32, 32, 4 + R - 1, 1} -> K-major rows rho = hh*32 + w (128 B of
+    // channels each, 128 B swizzle); out-of-range positions / channels are zero-filled
+    if (elect_one()) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
+      tma_prefetch(&mapX);
+      long long pwait = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int n = t / tiles_img;
+        const int h0 = ((t % tiles_img) / tiles_w) * kNsRows;
+        const int w0 = (t % tiles_w) * valid_w;
+        for (int ck = 0; ck < nck; ++ck, ++it) {
+          const int st = it % STAGES;
+          const long long tw0 = trace ? clock64() : 0;
+          mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+          if (trace) pwait += clock64() - tw0;
+          mbar_arrive_expect_tx(&full[st], a_bytes);
+          tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * 32, w0, h0, n);
+        }
+      }
+      NS_TRACE(61, pwait);
+    }
+  } else if (warp == kMma) {
+    if (elect_one()) {
+      NS_TRACE(0, clock64());
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // W' is written by the preceding launch
+      NS_TRACE(1, clock64());
+      tma_prefetch(&mapW);
+      mbar_arrive_expect_tx(wbar, w_bytes);
+      for (int r = 0; r < R; ++r)
+        for (int ck = 0; ck < nck; ++ck)
+          for (int s = 0; s < S; ++s)
+            tma_load_3d(wsm + ((r * nck + ck) * S + s) * FN * 128, &mapW, wbar, ck * 32, 0, r * S + s);
+      mbar_wait(wbar, 0);
+      NS_TRACE(2, clock64());
+      long long fwait = 0;
+      const uint32_t idesc = instr_desc(2, 128, static_cast<uint32_t>(ncol), 0, 0);
+      const uint32_t w_addr = smem_u32(wsm), a_base = smem_u32(asm_);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
+        if (local < 4) NS_TRACE(3 + 2 * local, clock64());
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ncol;
+        bool first = true;
+        for (int ck = 0; ck < nck; ++ck, ++it) {
+          const int st = it % STAGES;
+          const long long tw0 = trace ? clock64() : 0;
+          mbar_wait(&full[st], (it / STAGES) & 1);
+          if (trace) fwait += clock64() - tw0;
+          tc_fence_after();
+          const uint32_t a_addr = a_base + st * a_bytes;
+          for (int r = 0; r < R; ++r) {
+            const uint32_t wb = w_addr + (r * nck + ck) * ncol * 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              mma_tf32(d, smem_desc_sw128(a_addr + r * 4096 + k * 32, 16, 1024),
+                       smem_desc_sw128(wb + k * 32, 16, 1024), idesc, first ? 0u : 1u);
+              first = false;
+            }
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&acc_full[acc]);
+        if (local < 4) NS_TRACE(4 + 2 * local, clock64());
+      }
+      NS_TRACE(60, fwait);
+    }
+  } else {
+    // ---- epilogue: warp q owns TMEM lanes 32q.. = tile row q; lane = input column w0 + lane.
+    // out(w) = sum_s D[lane w + s][s*FN + f]: TMEM column block s of the neighbour s lanes down
+    const int q = warp & 3;
+    const int64_t fstride = static_cast<int64_t>(OH) * OW;
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int n = t / tiles_img;
+      const int h = ((t % tiles_img) / tiles_w) * kNsRows + q;
+      const int w = (t % tiles_w) * valid_w + lane;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const bool ok = lane < valid_w && n < N && h < OH && w < OW;
+      float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
+#pragma unroll 1
+      for (int c0 = 0; c0 < FN; c0 += 32) {
+        uint32_t r0[32], r1[32], r2[32];
+        const uint32_t base = tmem + acc * ncol + (static_cast<uint32_t>(q * 32) << 16) + c0;
+        tmem_ld32(base, r0);
+        if (S > 1) tmem_ld32(base + FN, r1);
+        if (S > 2) tmem_ld32(base + 2 * FN, r2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float v = __uint_as_float(r0[j]);
+          const float v1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1);
+          const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
+          if (S > 1) v += v1;
+          if (S > 2) v += v2;
+          // default write-back caching: neighbouring tiles complete the partial sectors in L2
+          if (ok && c0 + j < F) obase[(c0 + j) * fstride] = v;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (warp == kMma + 1 && lane == 0 && local < 4) NS_TRACE(40 + local, clock64());
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    tc_fence_after();
+    if (2 * ncol > 256) tmem_dealloc<512>(tmem);
+    else tmem_dealloc<256>(tmem);
+  }
+}
+
+void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
+  int FN = 32;
+  while (FN < a.F) FN *= 2;
+  const int nck = (a.C + 31) / 32;
+  const size_t w_bytes = static_cast<size_t>(a.R) * nck * a.S * FN * 128;
+  const size_t a_bytes = static_cast<size_t>(kNsRows + a.R - 1) * 4096;
+  // output columns per tile: at most 32 - (S - 1), balanced over the row (56 -> 2 x 28)
+  const int vmax = kNsCols - (a.S - 1);
+  const int tiles_w = (a.OW + vmax - 1) / vmax;
+  const int valid_w = (a.OW + tiles_w - 1) / tiles_w;
+  const int tiles_h = (a.OH + kNsRows - 1) / kNsRows;
+  const int total = a.N * tiles_h * tiles_w;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  int stages = static_cast<int>((budget - w_bytes) / a_bytes);
+  if (stages > 6) stages = 6;
+  const int grid = std::min(total, a.sms);
+  if (!a.maps_ready) {
+    const uint64_t dw[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.F), static_cast<uint64_t>(a.R) * a.S};
+    const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * 4, static_cast<uint64_t>(a.C) * a.F * 4};
+    const uint32_t bw[3] = {32, static_cast<uint32_t>(FN), 1};
+    encode_map(&a.mapW, false, true, a.ws_w, 3, dw, sw, bw);
+    // NHWC copy viewed as (c, w, h, n): box {32, 32, 4 + R - 1, 1} -> rows hh*32 + w
+    const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.H),
+                            static_cast<uint64_t>(a.N)};
+    const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * 4, static_cast<uint64_t>(a.W) * a.C * 4,
+                            static_cast<uint64_t>(a.H) * a.W * a.C * 4};
+    const uint32_t bx[4] = {32, kNsCols, static_cast<uint32_t>(kNsRows + a.R - 1), 1};
+    encode_map(&a.mapX, false, true, a.ws_x, 4, dx, sx, bx);
+    a.maps_ready = true;
+  }
+  auto launch = [&](auto kern) {
+    const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + 256;
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "conv_ns smem attribute");
+    mk.mark(st);
+    const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
+    const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
+    const size_t pre_smem = static_cast<size_t>(a.C) * (kBandRows * a.W + 1) * sizeof(float);
+    check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(pre_smem)),
+               "prepass smem attribute");
+    k_conv_prepass<float><<<a.N * ((a.H + kBandRows - 1) / kBandRows) + wblocks, 256, pre_smem, st>>>(
+        I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S);
+    check_cuda(cudaGetLastError(), "conv filter conversion launch");
+    count_launch();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
+    static long long* trace = nullptr;
+    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
+    if (trace) check_cuda(cudaMemsetAsync(trace, 0, 1024 * 64 * sizeof(long long), st), "trace");
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, O, a.N, a.C, a.H, a.W, a.F, FN, a.R, a.S, a.OH, a.OW,
+                                  tiles_h, tiles_w, total, valid_w, trace),
+               "conv_ns launch");
+    if (trace) {  // developer path: synchronous dump of the last launch
+      std::vector<long long> h(static_cast<size_t>(grid) * 64);
+      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
+      if (FILE* f = std::fopen(trace_path, "w")) {
+        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
+        std::fclose(f);
+      }
+    }
+    mk.mark(st);
+    count_launch();
+  };
+  switch (stages) {
+    case 2: launch(k_conv_ns<2>); break;
+    case 3: launch(k_conv_ns<3>); break;
+    case 4: launch(k_conv_ns<4>); break;
+    case 5: launch(k_conv_ns<5>); break;
+    case 6: launch(k_conv_ns<6>); break;
+    default: throw Error(Code::Unsupported, "conv_ns: filter bank does not fit in shared memory");
+  }
+}
 }  // namespace
 
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16) {
@@ -417,10 +683,22 @@ bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channel
   return static_cast<size_t>(C) * (kBandRows * W + 1) * sizeof(float) <= 96 * 1024;
 }
 
+bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16) {
+  int FN = 32;
+  while (FN < F) FN *= 2;
+  const size_t w_bytes = static_cast<size_t>(R) * ((C + 31) / 32) * S * FN * 128;
+  return !bf16 && stride == 1 && S >= 1 && S <= 3 && R >= 1 && R <= 8 && S * FN <= 256 &&
+         w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 1024 - 256;
+}
+
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {
   const float* i = static_cast<const float*>(I);
   const float* k = static_cast<const float*>(K);
   float* o = static_cast<float*>(O);
+  if (a.ns) {
+    run_conv_ns(a, i, k, o, st, mk);
+    return;
+  }
   int FN = 32;
   while (FN < a.F) FN *= 2;
   if (a.bf16) {

@@ -200,10 +200,21 @@ bool gemm_tc_ok(const OpDesc& op, bool bf16) {
                            static_cast<int>(op.param("K")), op.dtype_bytes);
 }
 
+// conv_ns (tf32, stride 1, S <= 3, S*F <= 256): NCHW in place, filter columns folded into N
+bool conv_ns_ok(const OpDesc& op, bool bf16) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16) return false;
+  if (std::getenv("GENSOR_CONV_NS") && std::string(std::getenv("GENSOR_CONV_NS")) == "0") return false;  // A/B
+  return conv_ns_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
+                           static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
+                           static_cast<int>(op.stride), bf16) &&
+         conv_tc_prepass_fits(static_cast<int>(op.param("C")), static_cast<int>(op.param("W")));
+}
+
 bool conv_tc_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4) return false;
   // conv_tc pays an NHWC pre-pass and wins through filter-row reuse: only for windows (R >= 2)
   if (op.param("R") < 2 && !bf16) return false;  // (bf16: conv_gemm has no bf16 path)
+  if (conv_ns_ok(op, bf16)) return true;
   return conv_tc_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
                            static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
                            static_cast<int>(op.stride), bf16) &&
@@ -342,16 +353,28 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.sms = sms;
           const size_t es = bf16 ? 2 : 4;
           const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
+          c.ns = conv_ns_ok(op, bf16);
           const size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
           check_cuda(cudaMalloc(&k->ws, ((wb + 255) & ~size_t(255)) + xb), "conv workspace");
           c.ws_w = k->ws;
           c.ws_x = static_cast<char*>(k->ws) + ((wb + 255) & ~size_t(255));
           k->launches = 2;  // filter conversion + conv (programmatic dependent launch), timed as one span
-          k->launch_names = {"conv_tc"};
-          const int tiles = ((c.N + 1) / 2) * ((c.OH + 7) / 8) * ((c.OW + 7) / 8);
-          pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F
-             << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
-             << ",\"block\":416,\"launches\":2,\"im2col\":\"in-kernel from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
+          k->launch_names = {c.ns ? "conv_ns" : "conv_tc"};
+          if (c.ns) {
+            const int tw = (c.OW + 32 - c.S) / (33 - c.S);
+            const int vw = (c.OW + tw - 1) / tw;
+            const int tiles = c.N * ((c.OH + 3) / 4) * tw;
+            int fn = 32;
+            while (fn < c.F) fn *= 2;
+            pi << "{\"family\":\"conv_ns\",\"M_tile\":\"4 rows x 32 input columns (" << vw
+               << " outputs)\",\"UMMA_N\":" << c.S * fn << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
+               << ",\"block\":192,\"launches\":2,\"A\":\"K-major TMA boxes from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
+          } else {
+            const int tiles = ((c.N + 1) / 2) * ((c.OH + 7) / 8) * ((c.OW + 7) / 8);
+            pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F
+               << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
+               << ",\"block\":192,\"launches\":2,\"A\":\"K-major TMA boxes from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
+          }
         } else if (conv_gemm_ok(op, bf16)) {
           k->family = Family::ConvGemm;
           k->launches = 2;  // filter conversion + conv (programmatic dependent launch), one span

@@ -408,16 +408,21 @@ void run_bn(GemmTcArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
-                const uint64_t* strides_bytes, const uint32_t* box, bool atom32) {
+void encode_map_swizzle(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
+                        const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle) {
   uint32_t elem_strides[5] = {1, 1, 1, 1, 1};
   CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                 : (tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
   CUresult r = encode_fn()(map, dt, rank, const_cast<void*>(ptr), dims, strides_bytes, box, elem_strides,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(Code::Cuda, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
+                const uint64_t* strides_bytes, const uint32_t* box, bool atom32) {
+  encode_map_swizzle(map, bf16, tf32, ptr, rank, dims, strides_bytes, box,
+                     atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 bool gemm_tc_supported(int M, int N, int K, int elem_bytes) {

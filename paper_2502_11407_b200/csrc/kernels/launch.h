@@ -57,6 +57,7 @@ struct ConvTcArgs {
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
   int sms = 148;
   bool bf16 = false;
+  bool ns = false;  // conv_ns: filter columns folded into the UMMA N (4 x 32 position tiles)
 };
 // ---- general tensor-core implicit-GEMM conv2d reading NCHW in place (conv_gemm.cu) ----
 struct ConvGemmArgs {
@@ -72,6 +73,7 @@ void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cu
 
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 bool conv_tc_prepass_fits(int C, int W);
+bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
 

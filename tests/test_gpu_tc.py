@@ -104,7 +104,9 @@ CONVS = [
     {"kind": "conv2d", "I": [2, 8, 12, 12], "K": [16, 8, 3, 3], "S": 1},
     {"kind": "conv2d", "I": [1, 32, 20, 40], "K": [64, 32, 3, 3], "S": 1},
     {"kind": "conv2d", "I": [2, 64, 10, 70], "K": [40, 64, 1, 1], "S": 1},  # 1x1, F not a power of two
-    {"kind": "conv2d", "I": [1, 16, 9, 35], "K": [64, 16, 5, 3], "S": 1},
+    {"kind": "conv2d", "I": [1, 16, 9, 35], "K": [64, 16, 5, 3], "S": 1},     # H*W % 4 != 0: NHWC copy
+    {"kind": "conv2d", "I": [3, 40, 13, 20], "K": [24, 40, 3, 3], "S": 1},    # ragged C, OW, odd N
+    {"kind": "conv2d", "I": [1, 24, 11, 12], "K": [96, 24, 2, 4], "S": 1},    # non-square window
 ]
 
 
@@ -113,7 +115,17 @@ CONVS = [
 def test_conv_tc(doc, variant, tol):
     info = check(doc, variant, tol)
     # 1x1 tf32 convs take the in-place implicit GEMM (no NHWC pre-pass), windows take conv_tc
-    assert info["plan"]["family"] == ("conv_gemm" if doc["K"][2] == 1 and variant == "tc_tf32" else "conv_tc")
+    F, S = doc["K"][0], doc["K"][3]
+    fn = 32
+    while fn < F:
+        fn *= 2
+    if variant == "tc_tf32" and doc["K"][2] == 1:
+        want = "conv_gemm"  # 1x1: the in-place implicit GEMM
+    elif variant == "tc_tf32" and S <= 3 and S * fn <= 256:
+        want = "conv_ns"    # NCHW in place, filter columns folded into the UMMA N
+    else:
+        want = "conv_tc"    # NHWC copy + TMA boxes
+    assert info["plan"]["family"] == want, info["plan"]
 
 
 @pytest.mark.parametrize("name,variant,tol", [("G", "tc_tf32", TF32_TOL), ("C", "tc_tf32", TF32_TOL),

@@ -69,12 +69,12 @@ __global__ void k_rate(long long* out, int iters) {
 
 // The conv_tc issue pattern: 4 rotating 20 KB A stages, each feeding 3 filter-row shifts (+2 KB)
 // x 4 k-steps against a resident 72 KB B bank (distinct operands every MMA).
-template <int N>
+template <int N, bool MNA>
 __global__ void k_rate_conv(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
-  constexpr uint32_t IDESC = instr_desc(2, 128, N, 0, 0);
+  constexpr uint32_t IDESC = instr_desc(2, 128, N, MNA ? 1 : 0, 0);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -86,16 +86,16 @@ __global__ void k_rate_conv(long long* out, int iters) {
   tc_fence_after();
   const uint32_t tmem = slot;
   if (threadIdx.x == 32) {
-    const uint32_t a = smem_u32(smem), b = a + 4 * 20480;
+    const uint32_t a = smem_u32(smem), b = a + 4 * 24576;
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      const uint32_t as = a + (i & 3) * 20480;
-      const uint32_t bs = b + (i % 6) * (3 * N * 128 / 2 > 12288 ? 0 : 0);
+      const uint32_t as = a + (i & 3) * 24576;
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          mma_tf32(tmem, smem_desc_sw128(as + r * 2048 + k * 32, 16, 1024),
-                   smem_desc_sw128(bs + (r * 6 + (i % 6)) * (N * 128) % (9 * N * 128) + k * 32, 16, 1024), IDESC, 1u);
+          mma_tf32(tmem, MNA ? smem_desc_sw128(as + r * 4096 + k * 1024, 4096, 512, 1)
+                             : smem_desc_sw128(as + r * 2048 + k * 32, 16, 1024),
+                   smem_desc_sw128(b + r * (N * 128) + k * 32, 16, 1024), IDESC, 1u);
     }
     mma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -196,18 +196,25 @@ int main() {
   rate<false, 128, true>(d, sms, "tf32 B MN-major");
   rate<true, 64, true>(d, sms, "bf16 B MN-major");
   rate<true, 256, true>(d, sms, "bf16 B MN-major");
-  {
+  auto conv_rate = [&](auto kern, int n, const char* name) {
     const int iters = 256;
-    const int smem = 4 * 20480 + 9 * 64 * 128;
-    CK(cudaFuncSetAttribute(k_rate_conv<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_rate_conv<64><<<sms, 64, smem>>>(d, iters);
+    const int smem = 4 * 24576 + 3 * n * 128;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<sms, 64, smem>>>(d, iters);
     CK(cudaDeviceSynchronize());
     long long h[256];
     CK(cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost));
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += h[i];
-    printf("tf32 N=64 conv pattern (distinct operands): %.1f cycles/MMA\n", avg / sms / (iters * 12.0));
-  }
+    printf("tf32 N=%d conv pattern, %s, distinct operands: %.1f cycles/MMA\n", n, name, avg / sms / (iters * 12.0));
+  };
+  conv_rate(k_rate_conv<64, false>, 64, "A K-major");
+  conv_rate(k_rate_conv<64, true>, 64, "A MN-major");
+  conv_rate(k_rate_conv<96, true>, 96, "A MN-major");
+  conv_rate(k_rate_conv<128, true>, 128, "A MN-major");
+  conv_rate(k_rate_conv<192, true>, 192, "A MN-major");
+  conv_rate(k_rate_conv<192, false>, 192, "A K-major");
+  conv_rate(k_rate_conv<256, true>, 256, "A MN-major");
   for (int k : {0, 1, 4, 12}) {
     CK(cudaFuncSetAttribute(k_commit_rtt, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     k_commit_rtt<<<sms, 64, 65536>>>(d, k, 64);
