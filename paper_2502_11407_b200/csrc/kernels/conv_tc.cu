@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const int h = ((t % tiles_img) / tiles_w) * kNsRows + q;
       const int w = (t % tiles_w) * valid_w + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      if (warp == kMma + 1 && lane == 0 && local < 4) NS_TRACE(44 + local, clock64());
       tc_fence_after();
       const bool ok = lane < valid_w && n < N && h < OH && w < OW;
       float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
