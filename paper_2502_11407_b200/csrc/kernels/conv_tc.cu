@@ -431,8 +431,9 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   uint8_t* asm_ = smem + w_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + STAGES * a_bytes);
   uint64_t* empty = full + STAGES;
+  constexpr int kWb = 8;  // filter-bank barriers: one per 32-channel chunk (the last takes the rest)
   uint64_t* wbar = empty + STAGES;
-  uint64_t* acc_full = wbar + 1;
+  uint64_t* acc_full = wbar + kWb;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(wbar, 1);
+    for (int i = 0; i < kWb; ++i) mbar_init(&wbar[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], kNsEpi);
@@ -491,12 +492,17 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");  // W' is written by the preceding launch
       NS_TRACE(1, clock64());
       tma_prefetch(&mapW);
-      mbar_arrive_expect_tx(wbar, w_bytes);
-      for (int r = 0; r < R; ++r)
-        for (int ck = 0; ck < nck; ++ck)
+      // chunk-major filter loads with a barrier per chunk: the first chunk's MMAs start once its
+      // R*S blocks have landed instead of after the whole bank
+      const uint32_t chunk_bytes = static_cast<uint32_t>(R * S * FN) * 128;
+      for (int ck = 0; ck < nck; ++ck) {
+        uint64_t* wb = &wbar[ck < kWb ? ck : kWb - 1];
+        if (ck < kWb - 1) mbar_arrive_expect_tx(wb, chunk_bytes);
+        else if (ck == kWb - 1) mbar_arrive_expect_tx(wb, chunk_bytes * static_cast<uint32_t>(nck - ck));
+        for (int r = 0; r < R; ++r)
           for (int s = 0; s < S; ++s)
-            tma_load_3d(wsm + ((r * nck + ck) * S + s) * FN * 128, &mapW, wbar, ck * 32, 0, r * S + s);
-      mbar_wait(wbar, 0);
+            tma_load_3d(wsm + ((r * nck + ck) * S + s) * FN * 128, &mapW, wb, ck * 32, 0, r * S + s);
+      }
       NS_TRACE(2, clock64());
       long long fwait = 0;
       const uint32_t idesc = instr_desc(2, 128, static_cast<uint32_t>(ncol), 0, 0);
@@ -514,6 +520,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           const long long tw0 = trace ? clock64() : 0;
           mbar_wait(&full[st], (it / STAGES) & 1);
           if (trace) fwait += clock64() - tw0;
+          if (local == 0 && ck < kWb) mbar_wait(&wbar[ck], 0);  // chunk ck's filters (last: the rest)
           tc_fence_after();
           const uint32_t a_addr = a_base + st * a_bytes;
           for (int r = 0; r < R; ++r) {
