@@ -230,6 +230,7 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
             e.synchronize()
             e2e_ms.append(s.elapsed_time(e))
         res["e2e_ms"] = e2e_ms
+        res["host_pipe"] = k.info.get("host_pipe")  # chunked H2D / kernel / D2H overlap, if used
         res["h2d"] = sum(x.numel() * x.element_size() for x in hin)
         res["d2h"] = hout.numel() * hout.element_size()
         if not torch.equal(hout.to(device), out):
@@ -722,7 +723,7 @@ def run_ours(args):
         "roofline": rl,
         "e2e": {"value": e2e_value, "unit": spec["unit"], "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
-                "path": "gensor_execute_host (pinned host buffers)"},
+                "path": "gensor_execute_host (pinned host buffers)", "pipeline": res.get("host_pipe")},
         "gpu_launches": res["launches"],
         "launch_breakdown_ms": {n: statistics.mean(v) for n, v in res["launch_ms"].items()},
         "construction_s": res["construct_s"],

@@ -2,6 +2,7 @@
 // This is the device replacement of the SPEC's lower()+interpret().
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <sstream>
 #include <cmath>
@@ -54,6 +55,21 @@ struct Kernel {
   // host-buffer execute staging (allocated on first use)
   void* d_in[3] = {nullptr, nullptr, nullptr};
   void* d_out = nullptr;
+  struct HostPipe* pipe = nullptr;  // chunked copy/compute overlap for execute_host (lazy)
+};
+
+// execute_host pipelining: the op is cut along an outer independent axis (conv/pool images,
+// GEMM batch or rows, GEMV/softmax rows) into chunks; chunk c's H2D copy, chunk c-1's kernels and
+// chunk c-2's D2H copy run concurrently on three streams (two copy engines + the SMs).
+struct HostPipe {
+  bool usable = false;
+  int64_t extent = 0, q = 0;  // split extent, chunk size (the last chunk may be smaller)
+  bool split[3] = {false, false, false};
+  size_t unit_bytes[4] = {0, 0, 0, 0};  // bytes per split unit: inputs 0..2, output (index 3)
+  Kernel* sub[2] = {nullptr, nullptr};  // kernels for chunk sizes q and the remainder
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k;
+  cudaEvent_t ev_shared = nullptr, ev_begin = nullptr;
 };
 
 namespace {
@@ -445,6 +461,16 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
 
 void destroy(Kernel* k) {
   if (!k) return;
+  if (HostPipe* hp = k->pipe) {
+    for (Kernel* sk : hp->sub) destroy(sk);
+    for (cudaEvent_t e : hp->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : hp->ev_k) cudaEventDestroy(e);
+    if (hp->ev_shared) cudaEventDestroy(hp->ev_shared);
+    if (hp->ev_begin) cudaEventDestroy(hp->ev_begin);
+    if (hp->s_in) cudaStreamDestroy(hp->s_in);
+    if (hp->s_out) cudaStreamDestroy(hp->s_out);
+    delete hp;
+  }
   for (void* p : k->d_in)
     if (p) cudaFree(p);
   if (k->d_out) cudaFree(k->d_out);
@@ -459,7 +485,11 @@ std::string info(const Kernel* k) {
   os << "{\"variant\":" << k->variant << ",\"variant_name\":\"" << kVariantNames[k->variant]
      << "\",\"op\":" << k->op.to_json() << ",\"state\":" << k->state.to_json(k->op)
      << ",\"flops\":" << json::num(k->op.flops_true()) << ",\"bytes\":" << json::num(k->op.bytes_true())
-     << ",\"launches\":" << k->launches << ",\"plan\":" << k->plan_info << "}";
+     << ",\"launches\":" << k->launches << ",\"plan\":" << k->plan_info;
+  if (k->pipe && k->pipe->usable)  // execute_host pipeline (set up by the first host-buffer execute)
+    os << ",\"host_pipe\":{\"split_extent\":" << k->pipe->extent << ",\"chunk\":" << k->pipe->q
+       << ",\"chunks\":" << k->pipe->ev_in.size() << "}";
+  os << "}";
   return os.str();
 }
 
@@ -544,12 +574,197 @@ std::vector<std::pair<std::string, float>> timings(Kernel* k) {
   return out;
 }
 
+namespace {
+
+// The op with its split extent replaced (same JSON form as OpDesc::to_json).
+std::string chunk_json(const OpDesc& op, int64_t n) {
+  std::ostringstream os;
+  auto p = [&](const char* name) { return op.param(name); };
+  os << "{\"kind\":\"" << kind_name(op.kind) << "\"";
+  switch (op.kind) {
+    case Kind::Gemm:
+      if (op.batch > 1)
+        os << ",\"M\":" << p("M") << ",\"K\":" << p("K") << ",\"N\":" << p("N") << ",\"batch\":" << n;
+      else
+        os << ",\"M\":" << n << ",\"K\":" << p("K") << ",\"N\":" << p("N");
+      break;
+    case Kind::Gemv:
+    case Kind::Softmax:
+      os << ",\"M\":" << n << ",\"N\":" << p("N");
+      break;
+    case Kind::Conv2d:
+      os << ",\"I\":[" << n << "," << p("C") << "," << p("H") << "," << p("W") << "],\"K\":[" << p("F") << ","
+         << p("C") << "," << p("R") << "," << p("S") << "],\"S\":" << op.stride;
+      break;
+    case Kind::DwConv2d:
+      os << ",\"I\":[" << n << "," << p("C") << "," << p("H") << "," << p("W") << "],\"K\":[" << p("C") << ",1,"
+         << p("R") << "," << p("S") << "],\"S\":" << op.stride;
+      break;
+    case Kind::AvgPool2d:
+      os << ",\"I\":[" << n << "," << p("C") << "," << p("H") << "," << p("W") << "],\"F\":" << p("F")
+         << ",\"S\":" << op.stride;
+      break;
+  }
+  os << ",\"dtype_bytes\":" << op.dtype_bytes << "}";
+  return os.str();
+}
+
+// The state's tiles clamped to the chunk's padded extents: a complete state of the chunk op with
+// the same reduce-axis walk (only the split spatial axis shrinks).
+Sched clamp_state(const Sched& s, const OpDesc& op) {
+  Sched c = s;
+  for (int a = 0; a < op.naxes; ++a) {
+    for (int l = 0; l < c.L; ++l) c.tiles[a][l] = std::min(c.tiles[a][l], op.ax[a].padded);
+    if (c.L > 0) c.vts[a] = std::min(c.vts[a], c.tiles[a][c.L - 1]);
+  }
+  return c;
+}
+
+void plan_pipe(Kernel* k) {
+  auto* hp = new HostPipe;
+  k->pipe = hp;
+  const OpDesc& op = k->op;
+  const int nin = op.input_count();
+  size_t total = 0;
+  for (int t = 0; t <= nin; ++t) total += tensor_bytes(op, t);
+  static const bool off = std::getenv("GENSOR_HOST_PIPE") && std::getenv("GENSOR_HOST_PIPE")[0] == '0';
+  if (off || total < (size_t(8) << 20)) return;  // small ops: one copy, one launch, one copy
+  switch (op.kind) {
+    case Kind::Gemm:
+      hp->extent = op.batch > 1 ? op.batch : op.param("M");
+      hp->split[0] = true;
+      hp->split[1] = op.batch > 1;
+      break;
+    case Kind::Gemv:
+    case Kind::Softmax:
+      hp->extent = op.param("M");
+      hp->split[0] = true;
+      break;
+    case Kind::Conv2d:
+    case Kind::DwConv2d:
+    case Kind::AvgPool2d:
+      hp->extent = op.param("N");
+      hp->split[0] = true;
+      break;
+  }
+  if (hp->extent < 2) return;
+  // chunks of ~9 MB of traffic (measured: PCIe reaches full duplex only for multi-MB copies), <= 16
+  static const int chunk_mb = std::getenv("GENSOR_HOST_PIPE_MB") ? std::atoi(std::getenv("GENSOR_HOST_PIPE_MB")) : 9;
+  int64_t chunks = std::min<int64_t>({hp->extent, 16, static_cast<int64_t>(total / (size_t(std::max(1, chunk_mb)) << 20))});
+  if (chunks < 2) return;
+  hp->q = (hp->extent + chunks - 1) / chunks;
+  if (op.kind == Kind::Gemm && op.batch == 1) hp->q = (hp->q + 127) / 128 * 128;  // whole 128-row M tiles
+  if (hp->q >= hp->extent) return;
+  for (int t = 0; t <= nin; ++t) {
+    const bool sp = t == nin || hp->split[t];
+    hp->unit_bytes[t == nin ? 3 : t] = sp ? tensor_bytes(op, t) / static_cast<size_t>(hp->extent) : 0;
+  }
+  const int64_t rem = hp->extent % hp->q;
+  for (int i = 0; i < (rem ? 2 : 1); ++i) {
+    const OpDesc cop = OpDesc::parse_text(chunk_json(op, i == 0 ? hp->q : rem));
+    hp->sub[i] = prepare(cop, clamp_state(k->state, cop), k->variant);
+  }
+  check_cuda(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking), "pipe stream");
+  check_cuda(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking), "pipe stream");
+  const int64_t n = (hp->extent + hp->q - 1) / hp->q;
+  hp->ev_in.resize(static_cast<size_t>(n));
+  hp->ev_k.resize(static_cast<size_t>(n));
+  for (int64_t c = 0; c < n; ++c) {
+    check_cuda(cudaEventCreateWithFlags(&hp->ev_in[static_cast<size_t>(c)], cudaEventDisableTiming), "pipe event");
+    check_cuda(cudaEventCreateWithFlags(&hp->ev_k[static_cast<size_t>(c)], cudaEventDisableTiming), "pipe event");
+  }
+  check_cuda(cudaEventCreateWithFlags(&hp->ev_shared, cudaEventDisableTiming), "pipe event");
+  check_cuda(cudaEventCreateWithFlags(&hp->ev_begin, cudaEventDisableTiming), "pipe event");
+  hp->usable = true;
+}
+
+}  // namespace
+
 void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, void* stream) {
   const OpDesc& op = k->op;
   if (n_in != op.input_count())
     throw Error(Code::ShapeMismatch,
                 "expected " + std::to_string(op.input_count()) + " inputs, got " + std::to_string(n_in));
   auto st = static_cast<cudaStream_t>(stream);
+  if (!k->pipe) {
+    try {
+      plan_pipe(k);
+    } catch (const Error& e) {  // a chunk shape the family cannot run: keep the one-shot path
+      if (std::getenv("GENSOR_HOST_PIPE_DEBUG")) std::fprintf(stderr, "host pipe disabled: %s\n", e.what());
+      if (k->pipe) {
+        for (Kernel*& sk : k->pipe->sub) {
+          destroy(sk);
+          sk = nullptr;
+        }
+        k->pipe->usable = false;
+      }
+    }
+  }
+  if (k->pipe && k->pipe->usable) {
+    HostPipe& hp = *k->pipe;
+    for (int i = 0; i < n_in; ++i)
+      if (!k->d_in[i]) check_cuda(cudaMalloc(&k->d_in[i], tensor_bytes(op, i)), "cudaMalloc input staging");
+    if (!k->d_out) check_cuda(cudaMalloc(&k->d_out, tensor_bytes(op, op.output_index())), "cudaMalloc output staging");
+    static const bool dbg = std::getenv("GENSOR_HOST_PIPE_DEBUG") != nullptr;
+    std::vector<cudaEvent_t> dev_t(dbg ? 3 * hp.ev_in.size() : 0);
+    cudaEvent_t dev_t0 = nullptr;
+    if (dbg) {
+      for (auto& e : dev_t) cudaEventCreate(&e);
+      cudaEventCreate(&dev_t0);
+      cudaEventRecord(dev_t0, st);
+    }
+    // order after prior work on the caller's stream, then the unsplit (shared) inputs
+    check_cuda(cudaEventRecord(hp.ev_begin, st), "pipe event");
+    check_cuda(cudaStreamWaitEvent(hp.s_in, hp.ev_begin, 0), "pipe wait");
+    check_cuda(cudaStreamWaitEvent(hp.s_out, hp.ev_begin, 0), "pipe wait");
+    for (int i = 0; i < n_in; ++i)
+      if (!hp.split[i])
+        check_cuda(cudaMemcpyAsync(k->d_in[i], h_in[i], tensor_bytes(op, i), cudaMemcpyHostToDevice, hp.s_in), "H2D");
+    check_cuda(cudaEventRecord(hp.ev_shared, hp.s_in), "pipe event");
+    check_cuda(cudaStreamWaitEvent(st, hp.ev_shared, 0), "pipe wait");
+    const int64_t n = static_cast<int64_t>(hp.ev_in.size());
+    for (int64_t c = 0; c < n; ++c) {
+      const int64_t u0 = c * hp.q, cnt = std::min(hp.q, hp.extent - u0);
+      Kernel* sk = hp.sub[cnt == hp.q ? 0 : 1];
+      const void* din[3] = {nullptr, nullptr, nullptr};
+      for (int i = 0; i < n_in; ++i) {
+        if (hp.split[i]) {
+          const size_t off = static_cast<size_t>(u0) * hp.unit_bytes[i], b = static_cast<size_t>(cnt) * hp.unit_bytes[i];
+          check_cuda(cudaMemcpyAsync(static_cast<char*>(k->d_in[i]) + off, static_cast<const char*>(h_in[i]) + off, b,
+                                     cudaMemcpyHostToDevice, hp.s_in),
+                     "H2D chunk");
+          din[i] = static_cast<char*>(k->d_in[i]) + off;
+        } else {
+          din[i] = k->d_in[i];
+        }
+      }
+      check_cuda(cudaEventRecord(hp.ev_in[static_cast<size_t>(c)], hp.s_in), "pipe event");
+      if (dbg) cudaEventRecord(dev_t[3 * c], hp.s_in);
+      check_cuda(cudaStreamWaitEvent(st, hp.ev_in[static_cast<size_t>(c)], 0), "pipe wait");
+      const size_t ooff = static_cast<size_t>(u0) * hp.unit_bytes[3], ob = static_cast<size_t>(cnt) * hp.unit_bytes[3];
+      execute(sk, din, n_in, static_cast<char*>(k->d_out) + ooff, st);
+      check_cuda(cudaEventRecord(hp.ev_k[static_cast<size_t>(c)], st), "pipe event");
+      if (dbg) cudaEventRecord(dev_t[3 * c + 1], st);
+      check_cuda(cudaStreamWaitEvent(hp.s_out, hp.ev_k[static_cast<size_t>(c)], 0), "pipe wait");
+      check_cuda(cudaMemcpyAsync(static_cast<char*>(h_out) + ooff, static_cast<char*>(k->d_out) + ooff, ob,
+                                 cudaMemcpyDeviceToHost, hp.s_out),
+                 "D2H chunk");
+      if (dbg) cudaEventRecord(dev_t[3 * c + 2], hp.s_out);
+    }
+    check_cuda(cudaStreamSynchronize(hp.s_out), "stream sync");
+    check_cuda(cudaStreamSynchronize(st), "stream sync");
+    if (dbg) {  // developer timeline: per chunk H2D done / kernels done / D2H done (us from begin)
+      for (int64_t c = 0; c < n; ++c) {
+        float t[3];
+        for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&t[j], dev_t0, dev_t[3 * c + j]);
+        std::fprintf(stderr, "chunk %lld: h2d %.1f  kernel %.1f  d2h %.1f\n", static_cast<long long>(c), t[0] * 1e3,
+                     t[1] * 1e3, t[2] * 1e3);
+      }
+      for (auto e : dev_t) cudaEventDestroy(e);
+      cudaEventDestroy(dev_t0);
+    }
+    return;
+  }
   for (int i = 0; i < n_in; ++i) {
     const size_t b = tensor_bytes(op, i);
     if (!k->d_in[i]) check_cuda(cudaMalloc(&k->d_in[i], b), "cudaMalloc input staging");

@@ -395,7 +395,11 @@ class Kernel:
         h = ctypes.c_void_p()
         _check(_lib.gensor_kernel_prepare(op._h, schedules._h, index, v, ctypes.byref(h)))
         self._h = h
-        self.info = _json_call(_lib.gensor_kernel_info, self._h)
+
+    @property
+    def info(self) -> dict:
+        """Plan, variant, work and (after the first host-buffer execute) the copy pipeline."""
+        return _json_call(_lib.gensor_kernel_info, self._h)
 
     def execute(self, inputs: Sequence[Any], output: Any, stream: Any = None) -> None:
         """Device execute: ``inputs``/``output`` are CUDA tensors (or raw device pointers);

@@ -1,7 +1,5 @@
 set -x
 mkdir -p gpurun_out
-C='{"kind":"conv2d","I":[16,64,58,58],"K":[64,64,3,3],"S":1}'
-timeout 600 python -m pytest tests/test_gpu_tc.py -x -q -k "conv or baseline" 2>&1 | tail -25 > gpurun_out/pytest_conv.log
-python tools/time_op.py "$C" tc_tf32 30 > gpurun_out/x_tc.log 2>&1
-GENSOR_PREPASS_PIPE=0 python tools/time_op.py "$C" tc_tf32 30 > gpurun_out/x_tc0.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 8 --csv --log-file gpurun_out/x_launches.csv python tools/time_op.py "$C" tc_tf32 2 > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_host_pipe.py tests/test_capi.py -x -q 2>&1 | tail -25 > gpurun_out/pytest_pipe.log
+timeout 600 python bench.py --steps 20 --warmup 5 --suite "" --no-cpu-baseline > gpurun_out/bench_conv2d.log 2>&1
+GENSOR_HOST_PIPE=0 timeout 600 python bench.py --steps 20 --warmup 5 --suite "" --no-cpu-baseline > gpurun_out/bench_conv2d_nopipe.log 2>&1
