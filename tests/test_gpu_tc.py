@@ -107,6 +107,8 @@ CONVS = [
     {"kind": "conv2d", "I": [1, 16, 9, 35], "K": [64, 16, 5, 3], "S": 1},     # H*W % 4 != 0: NHWC copy
     {"kind": "conv2d", "I": [3, 40, 13, 20], "K": [24, 40, 3, 3], "S": 1},    # ragged C, OW, odd N
     {"kind": "conv2d", "I": [1, 24, 11, 12], "K": [96, 24, 2, 4], "S": 1},    # non-square window
+    {"kind": "conv2d", "I": [2, 16, 12, 40], "K": [32, 16, 3, 2], "S": 1},    # S = 2: UMMA N = 64
+    {"kind": "conv2d", "I": [1, 48, 10, 70], "K": [128, 48, 3, 1], "S": 1},   # S = 1, F = 128: N = 128
 ]
 
 
