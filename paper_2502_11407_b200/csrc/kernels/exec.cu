@@ -237,6 +237,21 @@ bool conv_tc_ok(const OpDesc& op, bool bf16) {
          conv_tc_prepass_fits(static_cast<int>(op.param("C")), static_cast<int>(op.param("W")));
 }
 
+// 1x1 stride-1 conv (tf32) as a batched GEMM with the filter bank shared by the batch:
+// O[n] (F x P) = K (F x C) . I[n] (C x P) — the NCHW input is already the MN-major B operand and
+// the NCHW output the row-major C, so no pre-pass and no im2col (TMA strides: C, P multiples of 4).
+bool conv1x1_gemm_ok(const OpDesc& op, bool bf16) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16 || op.stride != 1) return false;
+  if (op.param("R") != 1 || op.param("S") != 1) return false;
+  if (std::getenv("GENSOR_CONV1X1_GEMM") && std::getenv("GENSOR_CONV1X1_GEMM")[0] == '0') return false;  // A/B
+  const int64_t P = op.param("H") * op.param("W");
+  // per-image N tiles of 128 positions: small planes (14x14 -> 77 % of the tile used) stay with
+  // conv_gemm, which flattens the positions of all images into M (measured on ResNet-50)
+  if (P < 512 && P % 128 != 0) return false;
+  return op.param("C") % 4 == 0 && P % 4 == 0 && gemm_tc_supported(static_cast<int>(op.param("F")), static_cast<int>(P),
+                                                                     static_cast<int>(op.param("C")), 4);
+}
+
 // General implicit-GEMM conv (tf32): any stride / window / channel count.
 bool conv_gemm_ok(const OpDesc& op, bool bf16) { return op.kind == Kind::Conv2d && op.dtype_bytes == 4 && !bf16; }
 
@@ -301,21 +316,30 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
       case 2:
       case 3: {
         const bool bf16 = k->variant == 3;
-        if (op.kind == Kind::Gemm && gemm_tc_ok(op, bf16)) {
+        const bool conv1x1 = conv1x1_gemm_ok(op, bf16);
+        if ((op.kind == Kind::Gemm && gemm_tc_ok(op, bf16)) || conv1x1) {
           k->family = Family::GemmTc;
           k->launch_names = {"gemm_tc"};
           GemmTcArgs& g = k->gemm;
-          g.M = static_cast<int>(op.param("M"));
-          g.N = static_cast<int>(op.param("N"));
-          g.K = static_cast<int>(op.param("K"));
-          g.batch = static_cast<int>(op.batch);
+          if (conv1x1) {  // O[n] = K . I[n]: M = F, N = H*W, K = C, batch = images, A shared
+            g.M = static_cast<int>(op.param("F"));
+            g.N = static_cast<int>(op.param("H") * op.param("W"));
+            g.K = static_cast<int>(op.param("C"));
+            g.batch = static_cast<int>(op.param("N"));
+            g.a_shared = true;
+          } else {
+            g.M = static_cast<int>(op.param("M"));
+            g.N = static_cast<int>(op.param("N"));
+            g.K = static_cast<int>(op.param("K"));
+            g.batch = static_cast<int>(op.batch);
+          }
           g.bf16 = bf16;
           // N tile from the schedule's level-1 n tile (UMMA N in [64, 256]); M tile = UMMA M 128
           // N tile: the schedule's level-1 n tile, clamped to the UMMA range [64, 256] (fp32 output:
           // [64, 128], the epilogue staging must fit next to the pipeline); halved while the grid
           // would leave SMs idle (fewer tiles than SMs).
           const int bn_max = bf16 ? 256 : 128;
-          int bn = static_cast<int>(pow2_clamp(s.L ? s.tile(op, 1, 1) : 128, 64, bn_max));
+          int bn = static_cast<int>(pow2_clamp(s.L && !conv1x1 ? s.tile(op, 1, 1) : 128, 64, bn_max));
           auto tiles = [&](int b) { return static_cast<int64_t>((g.M + 127) / 128) * ((g.N + b - 1) / b) * g.batch; };
           while (bn > 64 && tiles(bn) < sms) bn /= 2;
           if (const char* e = std::getenv("GENSOR_GEMM_BN")) bn = std::atoi(e);  // developer override
@@ -346,7 +370,8 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
               check_cuda(cudaMemset(g.flags, 0, static_cast<size_t>(t128) * 8), "gemm split-K flags");
             }
           }
-          pi << "{\"family\":\"gemm_tc\",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
+          pi << "{\"family\":\"gemm_tc\"" << (conv1x1 ? ",\"conv1x1\":\"O[n] = K . I[n], filter bank shared\"" : "")
+             << ",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
              << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true"
              << ",\"cluster_n\":" << g.cs << ",\"split_k\":" << g.splits << "}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16) &&
@@ -513,7 +538,11 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
       break;
     case Family::GemmTc:
       mk.mark(st);
-      launch_gemm_tc(k->gemm, d_in[0], d_in[1], d_out, st);
+      // 1x1 conv: inputs are (I, K) but the GEMM is K . I
+      if (k->gemm.a_shared)
+        launch_gemm_tc(k->gemm, d_in[1], d_in[0], d_out, st);
+      else
+        launch_gemm_tc(k->gemm, d_in[0], d_in[1], d_out, st);
       mk.mark(st);
       break;
     case Family::ConvTc:

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
               long long* __restrict__ trace, int splits, float* __restrict__ partials,
-              unsigned long long* __restrict__ flags, unsigned long long flag_target) {
+              unsigned long long* __restrict__ flags, unsigned long long flag_target, int a_batched) {
 #define GEMM_TRACE(slot, v) \
   if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int BM = 128;
@@ -133,10 +133,10 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* a_s = smem + s * STAGE;
           uint8_t* b_s = a_s + A_BYTES;
           if constexpr (CS > 1)  // this CTA's 1/CS row slice of A, to every CTA of the cluster
-            tma_load_3d_mc(a_s + rank * (A_BYTES / CS), &mapA, &full[s], kb * BK, m0 + rank * (BM / CS), b,
+            tma_load_3d_mc(a_s + rank * (A_BYTES / CS), &mapA, &full[s], kb * BK, m0 + rank * (BM / CS), b * a_batched,
                            static_cast<uint16_t>((1u << CS) - 1));
           else
-            tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
+            tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b * a_batched);  // 0: A shared by the batch
           (void)0;
 #pragma unroll
           for (int j = 0; j < B_CHUNKS; ++j)
@@ -332,7 +332,7 @@ void run_cs(GemmTcArgs& a, cudaStream_t st) {
     const int grid_u = std::min(units, a.sms);
     if (a.splits > 1) a.flag_target += 4ULL * (a.splits - 1);
     kern<<<grid_u, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total, trace, a.splits,
-                                    a.partials, a.flags, a.flag_target);
+                                    a.partials, a.flags, a.flag_target, a.a_shared ? 0 : 1);
     check_cuda(cudaGetLastError(), "gemm_tc launch");
     if (trace) {  // developer path: synchronous dump of the last launch
       std::vector<long long> h(static_cast<size_t>(grid) * 64);
@@ -358,7 +358,7 @@ void run_cs(GemmTcArgs& a, cudaStream_t st) {
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total,
                                   static_cast<long long*>(nullptr), 1, static_cast<float*>(nullptr),
-                                  static_cast<unsigned long long*>(nullptr), 0ULL),
+                                  static_cast<unsigned long long*>(nullptr), 0ULL, a.a_shared ? 0 : 1),
                "gemm_tc cluster launch");
   }
   count_launch();
@@ -434,7 +434,8 @@ void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaSt
   const int es = a.bf16 ? 2 : 4;
   const uint32_t bk = 128 / es;
   if (A != a.last_A || B != a.last_B) {
-    const uint64_t da[3] = {static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.batch)};
+    const uint64_t da[3] = {static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.M),
+                            static_cast<uint64_t>(a.a_shared ? 1 : a.batch)};
     const uint64_t sa[2] = {static_cast<uint64_t>(a.K) * es, static_cast<uint64_t>(a.K) * a.M * es};
     const uint32_t ba[3] = {bk, 128, 1};
     encode_map(&a.mapA, a.bf16, !a.bf16, A, 3, da, sa, ba);

@@ -43,6 +43,7 @@ struct GemmTcArgs {
   unsigned long long flag_target = 0;     // counter value the owners wait for in the last launch
   int sms = 148;
   bool bf16 = false;
+  bool a_shared = false;  // A is one matrix for every batch entry (1x1 conv: the filter bank)
 };
 bool gemm_tc_supported(int M, int N, int K, int elem_bytes);
 void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaStream_t st);

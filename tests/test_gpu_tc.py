@@ -121,8 +121,12 @@ def test_conv_tc(doc, variant, tol):
     fn = 32
     while fn < F:
         fn *= 2
-    if variant == "tc_tf32" and doc["K"][2] == 1:
-        want = "conv_gemm"  # 1x1: the in-place implicit GEMM
+    P = doc["I"][2] * doc["I"][3]
+    if (variant == "tc_tf32" and doc["K"][2] == 1 and doc["K"][3] == 1 and doc["I"][1] % 4 == 0 and P % 4 == 0
+            and (P >= 512 or P % 128 == 0)):
+        want = "gemm_tc"    # 1x1 stride 1: batched GEMM O[n] = K . I[n] on the NCHW tensors
+    elif variant == "tc_tf32" and doc["K"][2] == 1:
+        want = "conv_gemm"  # other 1x1: the in-place implicit GEMM
     elif variant == "tc_tf32" and S <= 3 and S * fn <= 256:
         want = "conv_ns"    # NCHW in place, filter columns folded into the UMMA N
     else:
@@ -162,3 +166,17 @@ GEMM_CONVS = [
 def test_conv_gemm_tf32(doc):
     info = check(doc, "tc_tf32", TF32_TOL)
     assert info["plan"]["family"] == "conv_gemm"
+
+
+# 1x1 stride-1 convs as batched GEMMs with the filter bank shared by the batch (gemm_tc, A_shared)
+CONV1X1 = [
+    {"kind": "conv2d", "I": [3, 64, 24, 30], "K": [256, 64, 1, 1], "S": 1},    # P = 720: ragged N tiles
+    {"kind": "conv2d", "I": [2, 256, 28, 28], "K": [64, 256, 1, 1], "S": 1},   # F = 64 < BM
+    {"kind": "conv2d", "I": [5, 36, 16, 32], "K": [200, 36, 1, 1], "S": 1},    # ragged F, C
+]
+
+
+@pytest.mark.parametrize("doc", CONV1X1, ids=lambda d: json.dumps(d["I"] + d["K"]))
+def test_conv1x1_gemm(doc):
+    info = check(doc, "tc_tf32", TF32_TOL)
+    assert info["plan"]["family"] == "gemm_tc" and "conv1x1" in info["plan"], info["plan"]
