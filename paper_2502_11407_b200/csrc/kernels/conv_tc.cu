@@ -412,12 +412,13 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
 //     with coalesced LDG and store them swizzled (the input rows are only 8 B aligned, which
 //     TMA cannot address); the filter bank is TMA-loaded once and stays resident.
 constexpr int kNsRows = 4, kNsCols = 32;
-constexpr int kNsEpi = 4;  // epilogue warps, one per TMEM lane quarter
+constexpr int kNsEpi = 8;  // epilogue warps: two per TMEM lane quarter, splitting the filter blocks
 constexpr int kNsThreads = 32 * (1 + 1 + kNsEpi);
 
 template <int STAGES>
 __global__ void __launch_bounds__(kNsThreads, 1)
-    k_conv_ns(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
+    k_conv_ns(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW,
+              const __grid_constant__ CUtensorMap mapO, int tma_store, float* __restrict__ O, int N,
               int C, int H, int W, int F, int FN, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
               int valid_w, long long* __restrict__ trace) {
   extern __shared__ uint8_t smem_raw[];
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   uint64_t* acc_full = wbar + kWb;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* stage_o = reinterpret_cast<float*>(smem + w_bytes + STAGES * a_bytes + 1024);  // [8 warps][8][32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_img = tiles_h * tiles_w;
 #define NS_TRACE(slot, v) \
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   } else {
     // ---- epilogue: warp q owns TMEM lanes 32q.. = tile row q; lane = input column w0 + lane.
     // out(w) = sum_s D[lane w + s][s*FN + f]: TMEM column block s of the neighbour s lanes down
-    const int q = warp & 3;
+    const int q = warp & 3, half = (warp - kMma - 1) >> 2;  // lane quarter, filter-block parity
     const int64_t fstride = static_cast<int64_t>(OH) * OW;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -556,29 +558,66 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const bool ok = lane < valid_w && n < N && h < OH && w < OW;
       float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
 #pragma unroll 1
-      for (int c0 = 0; c0 < FN; c0 += 32) {
+      for (int c0 = half * 32; c0 < FN + 32 * half; c0 += 64) {
+        if (c0 >= FN) {  // FN = 32: the second warp of the quarter has no block; release only
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          break;
+        }
         uint32_t r0[32], r1[32], r2[32];
         const uint32_t base = tmem + acc * ncol + (static_cast<uint32_t>(q * 32) << 16) + c0;
         tmem_ld32(base, r0);
         if (S > 1) tmem_ld32(base + FN, r1);
         if (S > 2) tmem_ld32(base + 2 * FN, r2);
         tmem_ld_wait();
+        if (c0 + 64 >= FN) {  // this warp's last TMEM block is in registers: hand the accumulator back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        }
+        if (tma_store) {
+          // four 8-filter quarters through this warp's staging slice [8 f][valid_w], each written
+          // to the NCHW output by one TMA store (clipped at the tensor edges)
+          float* stg = stage_o + ((warp - kMma - 1) * 8) * kNsCols;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float v = __uint_as_float(r0[j]);
-          const float v1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1);
-          const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
-          if (S > 1) v += v1;
-          if (S > 2) v += v2;
-          // default write-back caching: neighbouring tiles complete the partial sectors in L2
-          if (ok && c0 + j < F) obase[(c0 + j) * fstride] = v;
+          for (int hf = 0; hf < 4; ++hf) {
+            if (lane == 0) bulk_wait_read<0>();  // the previous store has read the slice
+            __syncwarp();
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = hf * 8 + jj;
+              float v = __uint_as_float(r0[j]);
+              const float v1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1);
+              const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
+              if (S > 1) v += v1;
+              if (S > 2) v += v2;
+              if (lane < valid_w) stg[jj * valid_w + lane] = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&mapO, stg, (t % tiles_w) * valid_w, ((t % tiles_img) / tiles_w) * kNsRows + q, c0 + hf * 8,
+                           n);
+              bulk_commit();
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float v = __uint_as_float(r0[j]);
+            const float v1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1);
+            const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
+            if (S > 1) v += v1;
+            if (S > 2) v += v2;
+            // default write-back caching: neighbouring tiles complete the partial sectors in L2
+            if (ok && c0 + j < F) obase[(c0 + j) * fstride] = v;
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
       if (warp == kMma + 1 && lane == 0 && local < 4) NS_TRACE(40 + local, clock64());
     }
+    if (tma_store && lane == 0) bulk_wait<0>();  // output stores complete before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -595,13 +634,17 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
   const int nck = (a.C + 31) / 32;
   const size_t w_bytes = static_cast<size_t>(a.R) * nck * a.S * FN * 128;
   const size_t a_bytes = static_cast<size_t>(kNsRows + a.R - 1) * 4096;
-  // output columns per tile: at most 32 - (S - 1), balanced over the row (56 -> 2 x 28)
-  const int vmax = kNsCols - (a.S - 1);
+  // output columns per tile: at most 32 - (S - 1), balanced over the row (56 -> 2 x 28); with
+  // 16 B-multiple output rows the epilogue stores through TMA, which needs valid_w % 4 == 0
+  const bool tma_store = a.OW % 4 == 0;
+  const int vmax = tma_store ? (kNsCols - (a.S - 1)) & ~3 : kNsCols - (a.S - 1);
   const int tiles_w = (a.OW + vmax - 1) / vmax;
-  const int valid_w = (a.OW + tiles_w - 1) / tiles_w;
+  int valid_w = (a.OW + tiles_w - 1) / tiles_w;
+  if (tma_store) valid_w = (valid_w + 3) & ~3;
   const int tiles_h = (a.OH + kNsRows - 1) / kNsRows;
   const int total = a.N * tiles_h * tiles_w;
-  const size_t budget = 227 * 1024 - 1024 - 256;
+  const size_t stage_o = kNsEpi * 8 * kNsCols * sizeof(float);  // epilogue staging (TMA-store path)
+  const size_t budget = 227 * 1024 - 2048 - stage_o;
   int stages = static_cast<int>((budget - w_bytes) / a_bytes);
   if (stages > 6) stages = 6;
   const int grid = std::min(total, a.sms);
@@ -619,8 +662,17 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     encode_map(&a.mapX, false, true, a.ws_x, 4, dx, sx, bx);
     a.maps_ready = true;
   }
+  if (tma_store && O != a.last_O) {  // NCHW output as (w, h, f, n): box {valid_w, 1, 16, 1}
+    const uint64_t dout[4] = {static_cast<uint64_t>(a.OW), static_cast<uint64_t>(a.OH), static_cast<uint64_t>(a.F),
+                              static_cast<uint64_t>(a.N)};
+    const uint64_t sout[3] = {static_cast<uint64_t>(a.OW) * 4, static_cast<uint64_t>(a.OH) * a.OW * 4,
+                              static_cast<uint64_t>(a.F) * a.OH * a.OW * 4};
+    const uint32_t bout[4] = {static_cast<uint32_t>(valid_w), 1, 8, 1};
+    encode_map_swizzle(&a.mapO, false, false, O, 4, dout, sout, bout, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.last_O = O;
+  }
   auto launch = [&](auto kern) {
-    const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + 256;
+    const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + stage_o + 1024;
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_ns smem attribute");
     mk.mark(st);
@@ -648,7 +700,7 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     static long long* trace = nullptr;
     if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
     if (trace) check_cuda(cudaMemsetAsync(trace, 0, 1024 * 64 * sizeof(long long), st), "trace");
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, O, a.N, a.C, a.H, a.W, a.F, FN, a.R, a.S, a.OH, a.OW,
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, a.mapO, tma_store ? 1 : 0, O, a.N, a.C, a.H, a.W, a.F, FN, a.R, a.S, a.OH, a.OW,
                                   tiles_h, tiles_w, total, valid_w, trace),
                "conv_ns launch");
     if (trace) {  // developer path: synchronous dump of the last launch
@@ -696,7 +748,7 @@ bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16) {
   while (FN < F) FN *= 2;
   const size_t w_bytes = static_cast<size_t>(R) * ((C + 31) / 32) * S * FN * 128;
   return !bf16 && stride == 1 && S >= 1 && S <= 3 && R >= 1 && R <= 8 && S * FN <= 256 &&
-         w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 1024 - 256;
+         w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
 }
 
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {

@@ -27,6 +27,8 @@ void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, 
 // ---- TMA tensor maps (gemm_tc.cu) ----
 void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
                 const uint64_t* strides_bytes, const uint32_t* box, bool atom32 = false);
+void encode_map_swizzle(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
+                        const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle);
 
 // ---- tensor-core GEMM family (gemm_tc.cu) ----
 struct GemmTcArgs {
@@ -59,6 +61,8 @@ struct ConvTcArgs {
   int sms = 148;
   bool bf16 = false;
   bool ns = false;  // conv_ns: filter columns folded into the UMMA N (4 x 32 position tiles)
+  CUtensorMap mapO;  // conv_ns: the NCHW output as (w, h, f, n) for TMA stores
+  const void* last_O = nullptr;
 };
 // ---- general tensor-core implicit-GEMM conv2d reading NCHW in place (conv_gemm.cu) ----
 struct ConvGemmArgs {
