@@ -226,21 +226,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   blocks [0, N*H)      NCHW row (n, h) -> NHWC X[n][h][:][:] through shared memory (coalesced
 //                        reads along w, 16 B writes along c);
 //   blocks [N*H, ...)    K[f][c][r][s] -> W'[r][s][f][c] (K-major B rows for the conv's TMA).
-constexpr int kBandRows = 2;  // pre-pass: input rows per block
+constexpr int kBandRows = 2;  // pre-pass: max input rows per block (shared-memory sizing)
+
+// rows per pre-pass block: 2 (measured: 1-row bands 10.7 us, 2-row 9.2 us for C; 464 B runs per
+// channel), GENSOR_PREPASS_BAND=1..4 for developer A/B
+int prepass_band(int W) {
+  static const int env = std::getenv("GENSOR_PREPASS_BAND") ? std::atoi(std::getenv("GENSOR_PREPASS_BAND")) : 0;
+  if (env >= 1 && env <= 4) return env;
+  (void)W;
+  return 2;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ I, const float* __restrict__ K,
                                                       T* __restrict__ X, T* __restrict__ Wt, int N, int C, int H,
-                                                      int W, int F, int RS) {
+                                                      int W, int F, int RS, int band) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  extern __shared__ float tile[];  // [C][W + 1]
-  // one block = a band of kBandRows input rows of one image, all channels: reads C contiguous
-  // runs of kBandRows*W floats (DRAM-page friendly), writes one contiguous NHWC slab
-  const int bands_per_img = (H + kBandRows - 1) / kBandRows;
+  extern __shared__ float tile[];  // [C][band*W + 1]
+  // one block = a band of `band` input rows of one image, all channels: reads C contiguous runs
+  // of band*W floats, writes one contiguous NHWC slab
+  const int bands_per_img = (H + band - 1) / band;
   const int rows = N * bands_per_img;
   if (static_cast<int>(blockIdx.x) < rows) {
-    const int n = blockIdx.x / bands_per_img, h0 = (blockIdx.x % bands_per_img) * kBandRows;
-    const int nr = min(kBandRows, H - h0);
+    const int n = blockIdx.x / bands_per_img, h0 = (blockIdx.x % bands_per_img) * band;
+    const int nr = min(band, H - h0);
     const int run = nr * W;           // floats per channel in this band
     const int pitch = run + 1;        // odd pitch: transposed reads are bank-conflict free
     const float* src = I + (static_cast<int64_t>(n) * C * H + h0) * W;
@@ -267,6 +276,29 @@ __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ 
             t[1] = v[u].y;
             t[2] = v[u].z;
             t[3] = v[u].w;
+          }
+        }
+      }
+    } else if ((reinterpret_cast<uintptr_t>(I) & 7) == 0 && run % 2 == 0 && (static_cast<int64_t>(H) * W) % 2 == 0 &&
+               (static_cast<int64_t>(h0) * W) % 2 == 0) {  // 8 B-aligned rows (even W): float2
+      const int r2 = run / 2;
+      for (int i0 = threadIdx.x; i0 < C * r2; i0 += 8 * 256) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 256;
+          const int c = i / r2, x = i - c * r2;
+          v[u] = i < C * r2 ? __ldg(reinterpret_cast<const float2*>(src + static_cast<int64_t>(c) * H * W) + x)
+                            : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 256;
+          const int c = i / r2, x = i - c * r2;
+          if (i < C * r2) {
+            float* t = tile + c * pitch + 2 * x;
+            t[0] = v[u].x;
+            t[1] = v[u].y;
           }
         }
       }
@@ -348,13 +380,14 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    const size_t pre_smem = static_cast<size_t>(a.C) * (kBandRows * a.W + 1) * sizeof(float);
+    const int band = prepass_band(a.W);
+    const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
     check_cuda(cudaFuncSetAttribute(k_conv_prepass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(pre_smem)),
                "prepass smem attribute");
-    k_conv_prepass<T><<<a.N * ((a.H + kBandRows - 1) / kBandRows) + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
+    k_conv_prepass<T><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
                                                                  static_cast<T*>(a.ws_w), a.N, a.C, a.H, a.W, a.F,
-                                                                 a.R * a.S);
+                                                                 a.R * a.S, band);
     check_cuda(cudaGetLastError(), "conv prepass launch");
     count_launch();
     static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
@@ -678,12 +711,13 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    const size_t pre_smem = static_cast<size_t>(a.C) * (kBandRows * a.W + 1) * sizeof(float);
+    const int band = prepass_band(a.W);
+    const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
     check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(pre_smem)),
                "prepass smem attribute");
-    k_conv_prepass<float><<<a.N * ((a.H + kBandRows - 1) / kBandRows) + wblocks, 256, pre_smem, st>>>(
-        I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S);
+    k_conv_prepass<float><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(
+        I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
     check_cuda(cudaGetLastError(), "conv filter conversion launch");
     count_launch();
     cudaLaunchConfig_t cfg = {};

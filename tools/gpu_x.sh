@@ -1,5 +1,4 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_sequences.py -x -q 2>&1 | tail -25 > gpurun_out/pytest_x.log
-timeout 600 python tools/sweep_seq.py resnet50 > gpurun_out/sweep_resnet.log 2>&1
-timeout 900 python bench.py --workload resnet50 --steps 3 --warmup 3 > gpurun_out/bench_resnet50.log 2>&1
+C='{"kind":"conv2d","I":[16,64,58,58],"K":[64,64,3,3],"S":1}'
+for b in 2 4; do GENSOR_PREPASS_BAND=$b python tools/time_op.py "$C" tc_tf32 30 > gpurun_out/x_b$b.log 2>&1; done
