@@ -1,4 +1,5 @@
 set -x
 mkdir -p gpurun_out
-C='{"kind":"conv2d","I":[16,64,58,58],"K":[64,64,3,3],"S":1}'
-for b in 2 4; do GENSOR_PREPASS_BAND=$b python tools/time_op.py "$C" tc_tf32 30 > gpurun_out/x_b$b.log 2>&1; done
+G='{"kind":"gemm","M":1024,"K":1024,"N":1024}'
+for cs in 1 2 4 8; do GENSOR_GEMM_CLUSTER=$cs python tools/time_op.py "$G" tc_tf32 30 > gpurun_out/g_cs$cs.log 2>&1; done
+GENSOR_GEMM_CLUSTER=8 timeout 300 python -m pytest tests/test_gpu_tc.py -x -q -k "gemm" 2>&1 | tail -3 > gpurun_out/pytest_g8.log
