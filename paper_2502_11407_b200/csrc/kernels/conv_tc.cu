@@ -22,6 +22,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "../host/error.hpp"
@@ -431,6 +432,62 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
 }
 
 
+// Space-to-depth pre-pass for stride-2 convs with few channels (the ResNet stem): blocks
+// [0, xblocks) write X2[n][h2][w2][(c, dy, dx)] = I[n][c][2 h2 + dy][2 w2 + dx] (0 outside), the
+// rest W2[r2][s2][f][(c, dy, dx)] = K[f][c][2 r2 + dy][2 s2 + dx] (0 past the window); conv_ns then
+// runs the equivalent stride-1 conv.
+__global__ void __launch_bounds__(256) k_s2d_prepass(const float* __restrict__ I, const float* __restrict__ K,
+                                                     float* __restrict__ X2, float* __restrict__ W2, int N, int C,
+                                                     int H, int W, int F, int R, int S, int H2, int Wd2, int R2,
+                                                     int S2, int xblocks) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int C2 = 4 * C;
+  if (static_cast<int>(blockIdx.x) < xblocks) {
+    // block = output rows (n, h2) for h2-row ids blockIdx.x, blockIdx.x + xblocks, ...: the two
+    // input rows of all C channels are read coalesced into shared memory, then the X2 row
+    // [w2][(c, dy, dx)] is written contiguously
+    extern __shared__ float rowsm[];  // [C][2][W]
+    for (int64_t rid = blockIdx.x; rid < static_cast<int64_t>(N) * H2; rid += xblocks) {
+      const int n = static_cast<int>(rid / H2), h2 = static_cast<int>(rid % H2);
+      // every (channel, row) load of this thread in flight at once (C <= 8: at most 16 rows)
+      const float* src = I + (static_cast<int64_t>(n) * C * H + 2 * h2) * W;
+      for (int w = threadIdx.x; w < W; w += 256) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int c = k >> 1, dy = k & 1;
+          v[k] = (c < C && 2 * h2 + dy < H) ? __ldg(src + (static_cast<int64_t>(c) * H + dy) * W + w) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if ((k >> 1) < C) rowsm[k * W + w] = v[k];
+      }
+      __syncthreads();
+      float* dst = X2 + rid * Wd2 * C2;
+      // thread = (output column w2, channel c): the 4 values (dy, dx) of one input channel form
+      // one 16 B store
+      for (int i = threadIdx.x; i < Wd2 * C; i += 256) {
+        const int c = i % C, w2 = i / C, w = 2 * w2;
+        const float* r0 = rowsm + (c * 2) * W;
+        const float4 v = make_float4(r0[w], w + 1 < W ? r0[w + 1] : 0.0f, r0[W + w], w + 1 < W ? r0[W + w + 1] : 0.0f);
+        *reinterpret_cast<float4*>(dst + static_cast<int64_t>(w2) * C2 + 4 * c) = v;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int64_t total = static_cast<int64_t>(R2) * S2 * F * C2;
+  const int nb = gridDim.x - xblocks;
+  for (int64_t e = (blockIdx.x - xblocks) * 256LL + threadIdx.x; e < total; e += static_cast<int64_t>(nb) * 256) {
+    const int c2 = static_cast<int>(e % C2);
+    const int f = static_cast<int>((e / C2) % F);
+    const int rs = static_cast<int>(e / (static_cast<int64_t>(C2) * F));
+    const int r2 = rs / S2, s2 = rs % S2;
+    const int c = c2 >> 2, r = 2 * r2 + ((c2 >> 1) & 1), sc = 2 * s2 + (c2 & 1);
+    W2[e] = (r < R && sc < S) ? __ldg(K + ((static_cast<int64_t>(f) * C + c) * R + r) * S + sc) : 0.0f;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // conv_ns: stride-1 tf32 conv with S*F <= 256, reading the NCHW input IN PLACE (no NHWC copy).
 //   * tile = 4 output rows x 32 columns of one image; the A operand is MN-major (32 consecutive
@@ -448,7 +505,7 @@ constexpr int kNsRows = 4, kNsCols = 32;
 constexpr int kNsEpi = 8;  // epilogue warps: two per TMEM lane quarter, splitting the filter blocks
 constexpr int kNsThreads = 32 * (1 + 1 + kNsEpi);
 
-template <int STAGES>
+template <int STAGES, int SMAX>
 __global__ void __launch_bounds__(kNsThreads, 1)
     k_conv_ns(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapO, int tma_store, float* __restrict__ O, int N,
@@ -558,10 +615,11 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           if (local == 0 && ck < kWb) mbar_wait(&wbar[ck], 0);  // chunk ck's filters (last: the rest)
           tc_fence_after();
           const uint32_t a_addr = a_base + st * a_bytes;
+          // k-steps of 8 channels that hold real channels (a 12-channel space-to-depth chunk: 2)
+          const int ksteps = min(4, (C - ck * 32 + 7) / 8);
           for (int r = 0; r < R; ++r) {
             const uint32_t wb = w_addr + (r * nck + ck) * ncol * 128;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < ksteps; ++k) {
               mma_tf32(d, smem_desc_sw128(a_addr + r * 4096 + k * 32, 16, 1024),
                        smem_desc_sw128(wb + k * 32, 16, 1024), idesc, first ? 0u : 1u);
               first = false;
@@ -598,11 +656,14 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           if (lane == 0) mbar_arrive(&acc_empty[acc]);
           break;
         }
-        uint32_t r0[32], r1[32], r2[32];
+        uint32_t r0[32], r1[32], r2[32], r3[SMAX > 3 ? 32 : 1];
         const uint32_t base = tmem + acc * ncol + (static_cast<uint32_t>(q * 32) << 16) + c0;
         tmem_ld32(base, r0);
         if (S > 1) tmem_ld32(base + FN, r1);
         if (S > 2) tmem_ld32(base + 2 * FN, r2);
+        if constexpr (SMAX > 3) {
+          if (S > 3) tmem_ld32(base + 3 * FN, r3);
+        }
         tmem_ld_wait();
         if (c0 + 64 >= FN) {  // this warp's last TMEM block is in registers: hand the accumulator back
           tc_fence_before();
@@ -625,6 +686,10 @@ __global__ void __launch_bounds__(kNsThreads, 1)
               const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
               if (S > 1) v += v1;
               if (S > 2) v += v2;
+              if constexpr (SMAX > 3) {
+                const float v3 = __shfl_down_sync(0xffffffffu, __uint_as_float(r3[j]), 3);
+                if (S > 3) v += v3;
+              }
               if (lane < valid_w) stg[jj * valid_w + lane] = v;
             }
             fence_proxy_async_smem();
@@ -643,6 +708,10 @@ __global__ void __launch_bounds__(kNsThreads, 1)
             const float v2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
             if (S > 1) v += v1;
             if (S > 2) v += v2;
+            if constexpr (SMAX > 3) {
+              const float v3 = __shfl_down_sync(0xffffffffu, __uint_as_float(r3[j]), 3);
+              if (S > 3) v += v3;
+            }
             // default write-back caching: neighbouring tiles complete the partial sectors in L2
             if (ok && c0 + j < F) obase[(c0 + j) * fstride] = v;
           }
@@ -664,13 +733,18 @@ __global__ void __launch_bounds__(kNsThreads, 1)
 void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
   int FN = 32;
   while (FN < a.F) FN *= 2;
-  const int nck = (a.C + 31) / 32;
-  const size_t w_bytes = static_cast<size_t>(a.R) * nck * a.S * FN * 128;
-  const size_t a_bytes = static_cast<size_t>(kNsRows + a.R - 1) * 4096;
+  // the kernel's problem: the op itself, or (stride 2) its space-to-depth form — a stride-1 conv
+  // over C2 = 4C channels (c, dy, dx) of ceil(H/2) x ceil(W/2) positions with ceil(R/2) x
+  // ceil(S/2) filters (K'[f][(c,dy,dx)][r'][s'] = K[f][c][2r'+dy][2s'+dx], 0 past the window)
+  const int gC = a.s2d ? 4 * a.C : a.C, gH = a.s2d ? (a.H + 1) / 2 : a.H, gW = a.s2d ? (a.W + 1) / 2 : a.W;
+  const int gR = a.s2d ? (a.R + 1) / 2 : a.R, gS = a.s2d ? (a.S + 1) / 2 : a.S;
+  const int nck = (gC + 31) / 32;
+  const size_t w_bytes = static_cast<size_t>(gR) * nck * gS * FN * 128;
+  const size_t a_bytes = static_cast<size_t>(kNsRows + gR - 1) * 4096;
   // output columns per tile: at most 32 - (S - 1), balanced over the row (56 -> 2 x 28); with
   // 16 B-multiple output rows the epilogue stores through TMA, which needs valid_w % 4 == 0
   const bool tma_store = a.OW % 4 == 0;
-  const int vmax = tma_store ? (kNsCols - (a.S - 1)) & ~3 : kNsCols - (a.S - 1);
+  const int vmax = tma_store ? (kNsCols - (gS - 1)) & ~3 : kNsCols - (gS - 1);
   const int tiles_w = (a.OW + vmax - 1) / vmax;
   int valid_w = (a.OW + tiles_w - 1) / tiles_w;
   if (tma_store) valid_w = (valid_w + 3) & ~3;
@@ -682,16 +756,16 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
   if (stages > 6) stages = 6;
   const int grid = std::min(total, a.sms);
   if (!a.maps_ready) {
-    const uint64_t dw[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.F), static_cast<uint64_t>(a.R) * a.S};
-    const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * 4, static_cast<uint64_t>(a.C) * a.F * 4};
+    const uint64_t dw[3] = {static_cast<uint64_t>(gC), static_cast<uint64_t>(a.F), static_cast<uint64_t>(gR) * gS};
+    const uint64_t sw[2] = {static_cast<uint64_t>(gC) * 4, static_cast<uint64_t>(gC) * a.F * 4};
     const uint32_t bw[3] = {32, static_cast<uint32_t>(FN), 1};
     encode_map(&a.mapW, false, true, a.ws_w, 3, dw, sw, bw);
     // NHWC copy viewed as (c, w, h, n): box {32, 32, 4 + R - 1, 1} -> rows hh*32 + w
-    const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.H),
+    const uint64_t dx[4] = {static_cast<uint64_t>(gC), static_cast<uint64_t>(gW), static_cast<uint64_t>(gH),
                             static_cast<uint64_t>(a.N)};
-    const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * 4, static_cast<uint64_t>(a.W) * a.C * 4,
-                            static_cast<uint64_t>(a.H) * a.W * a.C * 4};
-    const uint32_t bx[4] = {32, kNsCols, static_cast<uint32_t>(kNsRows + a.R - 1), 1};
+    const uint64_t sx[3] = {static_cast<uint64_t>(gC) * 4, static_cast<uint64_t>(gW) * gC * 4,
+                            static_cast<uint64_t>(gH) * gW * gC * 4};
+    const uint32_t bx[4] = {32, kNsCols, static_cast<uint32_t>(kNsRows + gR - 1), 1};
     encode_map(&a.mapX, false, true, a.ws_x, 4, dx, sx, bx);
     a.maps_ready = true;
   }
@@ -709,15 +783,24 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_ns smem attribute");
     mk.mark(st);
-    const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
+    const int64_t wt = static_cast<int64_t>(a.F) * gC * gR * gS;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    const int band = prepass_band(a.W);
-    const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
-    check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(pre_smem)),
-               "prepass smem attribute");
-    k_conv_prepass<float><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(
-        I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
+    if (a.s2d) {
+      const int xblocks = static_cast<int>(std::min<int64_t>(1 << 20, static_cast<int64_t>(a.N) * gH));  // a row per block
+      const size_t rsm = static_cast<size_t>(a.C) * 2 * a.W * sizeof(float);
+      check_cuda(cudaFuncSetAttribute(k_s2d_prepass, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)),
+                 "s2d smem attribute");
+      k_s2d_prepass<<<xblocks + wblocks, 256, rsm, st>>>(I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w),
+                                                       a.N, a.C, a.H, a.W, a.F, a.R, a.S, gH, gW, gR, gS, xblocks);
+    } else {
+      const int band = prepass_band(a.W);
+      const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
+      check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(pre_smem)),
+                 "prepass smem attribute");
+      k_conv_prepass<float><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(
+          I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
+    }
     check_cuda(cudaGetLastError(), "conv filter conversion launch");
     count_launch();
     cudaLaunchConfig_t cfg = {};
@@ -734,7 +817,7 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     static long long* trace = nullptr;
     if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
     if (trace) check_cuda(cudaMemsetAsync(trace, 0, 1024 * 64 * sizeof(long long), st), "trace");
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, a.mapO, tma_store ? 1 : 0, O, a.N, a.C, a.H, a.W, a.F, FN, a.R, a.S, a.OH, a.OW,
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, a.mapO, tma_store ? 1 : 0, O, a.N, gC, gH, gW, a.F, FN, gR, gS, a.OH, a.OW,
                                   tiles_h, tiles_w, total, valid_w, trace),
                "conv_ns launch");
     if (trace) {  // developer path: synchronous dump of the last launch
@@ -748,14 +831,23 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     mk.mark(st);
     count_launch();
   };
-  switch (stages) {
-    case 2: launch(k_conv_ns<2>); break;
-    case 3: launch(k_conv_ns<3>); break;
-    case 4: launch(k_conv_ns<4>); break;
-    case 5: launch(k_conv_ns<5>); break;
-    case 6: launch(k_conv_ns<6>); break;
-    default: throw Error(Code::Unsupported, "conv_ns: filter bank does not fit in shared memory");
-  }
+  auto pick = [&](auto smax) {
+    constexpr int SM = decltype(smax)::value;
+    switch (stages) {
+      case 2: launch(k_conv_ns<2, SM>); break;
+      case 3: launch(k_conv_ns<3, SM>); break;
+      case 4: launch(k_conv_ns<4, SM>); break;
+      case 5: launch(k_conv_ns<5, SM>); break;
+      case 6: launch(k_conv_ns<6, SM>); break;
+      default: throw Error(Code::Unsupported, "conv_ns: filter bank does not fit in shared memory");
+    }
+  };
+  // 4 filter columns need a fourth TMEM block in registers: a separate instantiation keeps the
+  // 3-column epilogue (the headline) free of its register pressure
+  if (gS > 3)
+    pick(std::integral_constant<int, 4>{});
+  else
+    pick(std::integral_constant<int, 3>{});
 }
 }  // namespace
 
@@ -777,11 +869,22 @@ bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channel
   return static_cast<size_t>(C) * (kBandRows * W + 1) * sizeof(float) <= 96 * 1024;
 }
 
+bool conv_s2d_supported(int C, int F, int R, int S, int stride, bool bf16) {
+  // stride-2, few channels: the space-to-depth form is a stride-1 conv_ns problem with 4C <= 32
+  // channels (one chunk) and ceil(S/2) <= 4 filter columns
+  int FN = 32;
+  while (FN < F) FN *= 2;
+  const int R2 = (R + 1) / 2, S2 = (S + 1) / 2;
+  const size_t w_bytes = static_cast<size_t>(R2) * S2 * FN * 128;
+  return !bf16 && stride == 2 && 4 * C <= 32 && C % 1 == 0 && (4 * C) % 4 == 0 && R2 >= 2 && R2 <= 8 && S2 <= 4 &&
+         S2 * FN <= 256 && w_bytes + 2 * static_cast<size_t>(kNsRows + R2 - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
+}
+
 bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16) {
   int FN = 32;
   while (FN < F) FN *= 2;
   const size_t w_bytes = static_cast<size_t>(R) * ((C + 31) / 32) * S * FN * 128;
-  return !bf16 && stride == 1 && S >= 1 && S <= 3 && R >= 1 && R <= 8 && S * FN <= 256 &&
+  return !bf16 && stride == 1 && S >= 1 && S <= 4 && R >= 1 && R <= 8 && S * FN <= 256 &&
          w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
 }
 

@@ -226,8 +226,18 @@ bool conv_ns_ok(const OpDesc& op, bool bf16) {
          conv_tc_prepass_fits(static_cast<int>(op.param("C")), static_cast<int>(op.param("W")));
 }
 
+// stride-2 convs with few channels (ResNet stem): conv_ns over the space-to-depth form
+bool conv_s2d_ok(const OpDesc& op, bool bf16) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16) return false;
+  if (std::getenv("GENSOR_CONV_S2D") && std::getenv("GENSOR_CONV_S2D")[0] == '0') return false;  // A/B
+  return conv_s2d_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
+                            static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
+                            static_cast<int>(op.stride), bf16);
+}
+
 bool conv_tc_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4) return false;
+  if (conv_s2d_ok(op, bf16)) return true;
   // conv_tc pays an NHWC pre-pass and wins through filter-row reuse: only for windows (R >= 2)
   if (op.param("R") < 2 && !bf16) return false;  // (bf16: conv_gemm has no bf16 path)
   if (conv_ns_ok(op, bf16)) return true;
@@ -393,23 +403,30 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.bf16 = bf16;
           c.sms = sms;
           const size_t es = bf16 ? 2 : 4;
-          const size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
-          c.ns = conv_ns_ok(op, bf16);
-          const size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
+          size_t wb = static_cast<size_t>(c.R) * c.S * c.F * c.C * es;
+          c.s2d = conv_s2d_ok(op, bf16);
+          c.ns = c.s2d || conv_ns_ok(op, bf16);
+          size_t xb = static_cast<size_t>(c.N) * c.H * c.W * c.C * es;
+          if (c.s2d) {  // X2 [N][H/2][W/2][4C] and W2 [R/2][S/2][F][4C]
+            xb = static_cast<size_t>(c.N) * ((c.H + 1) / 2) * ((c.W + 1) / 2) * 4 * c.C * es;
+            wb = static_cast<size_t>((c.R + 1) / 2) * ((c.S + 1) / 2) * c.F * 4 * c.C * es;
+          }
           check_cuda(cudaMalloc(&k->ws, ((wb + 255) & ~size_t(255)) + xb), "conv workspace");
           c.ws_w = k->ws;
           c.ws_x = static_cast<char*>(k->ws) + ((wb + 255) & ~size_t(255));
           k->launches = 2;  // filter conversion + conv (programmatic dependent launch), timed as one span
           k->launch_names = {c.ns ? "conv_ns" : "conv_tc"};
           if (c.ns) {
-            const int tw = (c.OW + 32 - c.S) / (33 - c.S);
+            const int gs = c.s2d ? (c.S + 1) / 2 : c.S;
+            const int tw = (c.OW + 32 - gs) / (33 - gs);
             const int vw = (c.OW + tw - 1) / tw;
             const int tiles = c.N * ((c.OH + 3) / 4) * tw;
             int fn = 32;
             while (fn < c.F) fn *= 2;
-            pi << "{\"family\":\"conv_ns\",\"M_tile\":\"4 rows x 32 input columns (" << vw
-               << " outputs)\",\"UMMA_N\":" << c.S * fn << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
-               << ",\"block\":192,\"launches\":2,\"A\":\"K-major TMA boxes from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
+            pi << "{\"family\":\"conv_ns\"" << (c.s2d ? ",\"space_to_depth\":\"stride 2 -> stride 1 over 4C channels\"" : "")
+               << ",\"M_tile\":\"4 rows x 32 input columns (" << vw
+               << " outputs)\",\"UMMA_N\":" << gs * fn << ",\"tiles\":" << tiles << ",\"grid\":" << std::min(tiles, sms)
+               << ",\"block\":320,\"launches\":2,\"A\":\"K-major TMA boxes from the NHWC pre-pass copy\",\"prepass\":\"NCHW->NHWC + K-major filters, PDL\"}";
           } else {
             const int tiles = ((c.N + 1) / 2) * ((c.OH + 7) / 8) * ((c.OW + 7) / 8);
             pi << "{\"family\":\"conv_tc\",\"M_tile\":\"8 rows x 2 images x 8 columns\",\"FN\":" << c.F

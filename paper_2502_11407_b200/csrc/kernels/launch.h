@@ -61,6 +61,7 @@ struct ConvTcArgs {
   int sms = 148;
   bool bf16 = false;
   bool ns = false;  // conv_ns: filter columns folded into the UMMA N (4 x 32 position tiles)
+  bool s2d = false;  // conv_ns over the space-to-depth form of a stride-2 conv (ResNet stem)
   CUtensorMap mapO;  // conv_ns: the NCHW output as (w, h, f, n) for TMA stores
   const void* last_O = nullptr;
 };
@@ -79,6 +80,7 @@ void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cu
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 bool conv_tc_prepass_fits(int C, int W);
 bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16);
+bool conv_s2d_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
 void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
 

@@ -127,7 +127,7 @@ def test_conv_tc(doc, variant, tol):
         want = "gemm_tc"    # 1x1 stride 1: batched GEMM O[n] = K . I[n] on the NCHW tensors
     elif variant == "tc_tf32" and doc["K"][2] == 1:
         want = "conv_gemm"  # other 1x1: the in-place implicit GEMM
-    elif variant == "tc_tf32" and S <= 3 and S * fn <= 256:
+    elif variant == "tc_tf32" and S <= 4 and S * fn <= 256:
         want = "conv_ns"    # NCHW in place, filter columns folded into the UMMA N
     else:
         want = "conv_tc"    # NHWC copy + TMA boxes
@@ -155,7 +155,6 @@ def test_auto_picks_tensor_cores():
 # the shapes conv_tc does not take — stride 2, ResNet stem (C=3, 7x7), F > 256, odd batch.
 GEMM_CONVS = [
     {"kind": "conv2d", "I": [2, 16, 17, 17], "K": [32, 16, 3, 3], "S": 2},
-    {"kind": "conv2d", "I": [3, 3, 23, 23], "K": [64, 3, 7, 7], "S": 2},       # stem: C=3 (padded to 4)
     {"kind": "conv2d", "I": [1, 64, 9, 9], "K": [300, 64, 1, 1], "S": 1},       # F > 256, ragged N tile
     {"kind": "conv2d", "I": [2, 96, 8, 8], "K": [128, 96, 1, 1], "S": 2},      # 1x1 stride-2 projection
     {"kind": "conv2d", "I": [1, 512, 9, 9], "K": [64, 512, 3, 3], "S": 1},     # large C: weights streamed
@@ -166,6 +165,21 @@ GEMM_CONVS = [
 def test_conv_gemm_tf32(doc):
     info = check(doc, "tc_tf32", TF32_TOL)
     assert info["plan"]["family"] == "conv_gemm"
+
+
+# stride-2 few-channel convs (the ResNet stem) through conv_ns on their space-to-depth form
+S2D = [
+    {"kind": "conv2d", "I": [3, 3, 23, 23], "K": [64, 3, 7, 7], "S": 2},      # stem shape, odd sizes
+    {"kind": "conv2d", "I": [2, 3, 229, 229], "K": [64, 3, 7, 7], "S": 2},    # ResNet-50 stem, batch 2
+    {"kind": "conv2d", "I": [2, 8, 30, 34], "K": [40, 8, 3, 3], "S": 2},      # 4C = 32 channels, F = 40
+    {"kind": "conv2d", "I": [1, 5, 17, 16], "K": [32, 5, 4, 2], "S": 2},      # even window, ragged 4C
+]
+
+
+@pytest.mark.parametrize("doc", S2D, ids=lambda d: json.dumps(d["I"] + d["K"]))
+def test_conv_s2d(doc):
+    info = check(doc, "tc_tf32", TF32_TOL)
+    assert info["plan"]["family"] == "conv_ns" and "space_to_depth" in info["plan"], info["plan"]
 
 
 # 1x1 stride-1 convs as batched GEMMs with the filter bank shared by the batch (gemm_tc, A_shared)
