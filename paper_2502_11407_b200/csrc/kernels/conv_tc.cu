@@ -1,20 +1,24 @@
-// Tensor-core implicit-GEMM conv2d (stride 1), instantiated from a constructed conv2d schedule:
-//   O[n][f][h][w] = sum_{c,r,s} I[n][c][h+r][w+s] * K[f][c][r][s]   (op_spec.cpp:177-181)
-// GEMM view: M = output positions, N = f, K = (r, s, c). Reference layouts in and out:
+// Tensor-core implicit-GEMM conv2d families, instantiated from a constructed conv2d schedule:
+//   O[n][f][h][w] = sum_{c,r,s} I[n][c][h*S+r][w*S+s] * K[f][c][r][s]   (op_spec.cpp:177-181)
+// GEMM view: M = output positions, N = f, K = (r, s, c). Reference layouts in and out.
 //
-//   * launch 1 (pre-pass): NCHW -> NHWC copy of the input (2-row bands, DRAM-page friendly) and
-//     the K-major filter bank W'[r][s][f][c]; it triggers the conv grid early (programmatic
-//     dependent launch), whose producers / MMA warp wait for it with griddepcontrol.wait;
-//   * output tile = 8 rows x 2 images x 8 columns = 128 positions (one UMMA M), laid out in shared
-//     memory as row rho = h*16 + img*8 + w. A shift by filter row r is then rho + 16r (2 KB, a
-//     whole number of 1 KB swizzle atoms), so ONE staged box of (8+R-1) x 2 x 8 positions per
-//     (s, 128 B channel chunk) serves all R row shifts (3x fewer staged bytes for 3x3). The tile
-//     divides 56 x 56 exactly: C = [16,64,58,58] is 392 tiles, no idle lanes;
-//   * one producer thread TMA-loads each (s, channel chunk) box straight into its stage: the NHWC
-//     copy is described by a 4-D tensor map whose dimensions are permuted to (c, w, n, h), so a
-//     box {chunk, 8, 2, 8+R-1} lands as rows rho = h*16 + img*8 + w, 128 B swizzled — the layout
-//     the MMA descriptors expect, no software producers; the filter bank is TMA-loaded into
-//     shared memory once and stays resident;
+// conv_ns (the configs[1] headline; stride 1, S <= 4, S*F <= 256):
+//   * launch 1 (pre-pass): NCHW -> NHWC copy of the input (2-row bands) and the K-major filter
+//     bank W'[r][s][f][c]; it triggers the conv grid early (programmatic dependent launch);
+//   * the filter columns s are folded into the UMMA N (N = S*F): one MMA multiplies each staged
+//     input position by all S columns at full tensor-core rate, and the epilogue adds TMEM block
+//     s of lane w + s into output w with warp shuffles — no s-shifted copies of A;
+//   * tile = 4 output rows x 32 input columns of one image; one TMA box {32 channels, 32 columns,
+//     4 + R - 1 rows} per 32-channel chunk (128 B swizzle); a filter-row shift r is +4 KB;
+//   * 8 epilogue warps (two per TMEM lane quarter) store through shared memory with TMA;
+//   * stride-2 few-channel convs (the ResNet stem) run as the equivalent stride-1 conv over the
+//     space-to-depth form (4C channels, ceil(R/2) x ceil(S/2) filters; k_s2d_prepass).
+//
+// conv_tc (other stride-1 windows, and the bf16 variant):
+//   * same pre-pass; output tile = 8 rows x 2 images x 8 columns laid out in shared memory as row
+//     rho = h*16 + img*8 + w, so a filter-row shift r is rho + 16r (2 KB, whole 1 KB swizzle
+//     atoms): ONE staged box of (8+R-1) x 2 x 8 positions per (s, 128 B channel chunk) serves all
+//     R row shifts; the box is one TMA load over a (c, w, n, h)-permuted view of the NHWC copy;
 //   * one thread issues tcgen05.mma (kind::tf32 or kind::f16) into two TMEM accumulators
 //     (double-buffered: the epilogue of tile i overlaps the MMAs of tile i+1);
 //   * 4 epilogue warps: tcgen05.ld -> streaming stores into NCHW.
@@ -876,7 +880,7 @@ bool conv_s2d_supported(int C, int F, int R, int S, int stride, bool bf16) {
   while (FN < F) FN *= 2;
   const int R2 = (R + 1) / 2, S2 = (S + 1) / 2;
   const size_t w_bytes = static_cast<size_t>(R2) * S2 * FN * 128;
-  return !bf16 && stride == 2 && 4 * C <= 32 && C % 1 == 0 && (4 * C) % 4 == 0 && R2 >= 2 && R2 <= 8 && S2 <= 4 &&
+  return !bf16 && stride == 2 && 4 * C <= 32 && R2 >= 2 && R2 <= 8 && S2 <= 4 &&
          S2 * FN <= 256 && w_bytes + 2 * static_cast<size_t>(kNsRows + R2 - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
 }
 
