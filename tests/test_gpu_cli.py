@@ -21,6 +21,8 @@ OPS = [
     ({"kind": "softmax", "M": 64, "N": 300}, ["auto"]),
     ({"kind": "avgpool2d", "I": [2, 8, 20, 20], "F": 3, "S": 1}, ["auto", "simt_parity"]),
     ({"kind": "dwconv2d", "I": [2, 8, 20, 20], "K": [8, 1, 3, 3], "S": 2}, ["auto"]),
+    ({"kind": "conv2d", "I": [2, 3, 37, 37], "K": [32, 3, 7, 7], "S": 2}, ["auto"]),     # space-to-depth
+    ({"kind": "conv2d", "I": [2, 32, 16, 32], "K": [96, 32, 1, 1], "S": 1}, ["auto"]),   # 1x1 as GEMM
 ]
 
 
