@@ -340,17 +340,28 @@ __global__ void __launch_bounds__(kSoftmaxThreads) k_softmax_warp(const float* _
   const int64_t nv = N >> 2;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t r_end = min(M, (u + 1) * rows_per_unit);
-    for (int64_t m = u * rows_per_unit + warp; m < r_end; m += kSoftmaxThreads / 32) {
-      const float* row = X + m * N;
+    constexpr int64_t kStep = kSoftmaxThreads / 32;
+    // software pipeline: the next row of this warp is in flight while the current one is reduced,
+    // exponentiated and stored
+    float4 nxt[VPL];
+    auto load_row = [&](int64_t m, float4 (&dst)[VPL]) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int64_t i = lane + 32 * q;
+        dst[q] = (m < r_end && i < nv) ? ld_stream4(X + m * N + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    load_row(u * rows_per_unit + warp, nxt);
+    for (int64_t m = u * rows_per_unit + warp; m < r_end; m += kStep) {
       float4 v[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) v[q] = nxt[q];
+      load_row(m + kStep, nxt);
       float mx = -INFINITY;
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const int64_t i = lane + 32 * q;
-        if (i < nv) {
-          v[q] = ld_stream4(row + 4 * i);
-          mx = fmaxf(mx, fmaxf(fmaxf(v[q].x, v[q].y), fmaxf(v[q].z, v[q].w)));
-        }
+        if (i < nv) mx = fmaxf(mx, fmaxf(fmaxf(v[q].x, v[q].y), fmaxf(v[q].z, v[q].w)));
       }
       mx = warp_max(mx);
       float ts = 0.0f;
