@@ -59,7 +59,7 @@ struct ConvTraits<__nv_bfloat16> {
   static constexpr bool kF16 = true;
 };
 
-template <typename T, int FN, int STAGES>
+template <typename T, int FN, int STAGES, bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
               int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
@@ -76,11 +76,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nck = (C + CK - 1) / CK;
   const int box_rows = (kTH + R - 1) * kTI * kTW;  // staged positions per (s, c-chunk)
-  const uint32_t w_bytes = static_cast<uint32_t>(R * S * nck) * W_CHUNK;
+  // STREAM: the filter bank does not fit next to the pipeline, so every stage carries its R
+  // filter-row blocks of W' (TMA) next to the A box instead of a resident bank
+  const uint32_t w_bytes = STREAM ? 0u : static_cast<uint32_t>(R * S * nck) * W_CHUNK;
   const uint32_t a_bytes = static_cast<uint32_t>(box_rows * 128);
+  const uint32_t stage_bytes = a_bytes + (STREAM ? static_cast<uint32_t>(R) * W_CHUNK : 0u);
   uint8_t* wsm = smem;
   uint8_t* asm_ = smem + w_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + STAGES * a_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + STAGES * stage_bytes);
   uint64_t* empty = full + STAGES;
   uint64_t* wbar = empty + STAGES;
   uint64_t* acc_full = wbar + 1;       // [2]
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
       tma_prefetch(&mapX);
+      if constexpr (STREAM) tma_prefetch(&mapW);
       long long pwait = 0;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -129,8 +133,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long tw0 = trace ? clock64() : 0;
             mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
             if (trace) pwait += clock64() - tw0;
-            mbar_arrive_expect_tx(&full[st], a_bytes);
-            tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * CK, w0 + s, n0, h0);
+            mbar_arrive_expect_tx(&full[st], stage_bytes);
+            tma_load_4d(asm_ + st * stage_bytes, &mapX, &full[st], ck * CK, w0 + s, n0, h0);
+            if constexpr (STREAM)
+              for (int r = 0; r < R; ++r)
+                tma_load_3d(asm_ + st * stage_bytes + a_bytes + r * W_CHUNK, &mapW, &full[st], ck * CK, 0, r * S + s);
           }
       }
       CONV_TRACE(61, pwait);
@@ -141,11 +148,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // W' is written by the preceding conversion launch (programmatic dependent launch: this
       // grid starts early and only this thread waits for the primary grid's results)
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      tma_prefetch(&mapW);
-      mbar_arrive_expect_tx(wbar, w_bytes);
-      for (int rs = 0; rs < R * S; ++rs)
-        for (int ck = 0; ck < nck; ++ck) tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
-      mbar_wait(wbar, 0);
+      if constexpr (!STREAM) {
+        tma_prefetch(&mapW);
+        mbar_arrive_expect_tx(wbar, w_bytes);
+        for (int rs = 0; rs < R * S; ++rs)
+          for (int ck = 0; ck < nck; ++ck) tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
+        mbar_wait(wbar, 0);
+      }
       CONV_TRACE(2, clock64());
       long long fwait = 0;
       const uint32_t w_addr = smem_u32(wsm);
@@ -165,9 +174,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[st], (it / STAGES) & 1);
             if (trace) fwait += clock64() - tw0;
             tc_fence_after();
-            const uint32_t a_addr = a_base + st * a_bytes;
+            const uint32_t a_addr = a_base + st * stage_bytes;
             for (int r = 0; r < R; ++r) {
-              const uint32_t wa = w_addr + ((r * S + s) * nck + ck) * W_CHUNK;
+              const uint32_t wa = STREAM ? a_addr + a_bytes + r * W_CHUNK : w_addr + ((r * S + s) * nck + ck) * W_CHUNK;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = smem_desc_sw128(a_addr + r * (kTI * kTW * 128) + k * 32, 16, 1024);
@@ -354,8 +363,12 @@ template <typename T, int FN>
 void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
   constexpr int CK = 128 / sizeof(T);
   const int nck = (a.C + CK - 1) / CK;
-  const size_t w_bytes = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
-  const size_t a_bytes = static_cast<size_t>((kTH + a.R - 1) * kTI * kTW * 128);
+  const size_t a_bytes0 = static_cast<size_t>((kTH + a.R - 1) * kTI * kTW * 128);
+  const size_t bank = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
+  // resident filter bank when it fits next to two A stages, else filter blocks streamed per stage
+  const bool stream = bank + 2 * a_bytes0 > 227 * 1024 - 1024 - 256;
+  const size_t w_bytes = stream ? 0 : bank;
+  const size_t a_bytes = a_bytes0 + (stream ? static_cast<size_t>(a.R) * FN * 128 : 0);
   const int tiles_h = (a.OH + kTH - 1) / kTH, tiles_w = (a.OW + kTW - 1) / kTW;
   const int total = ((a.N + kTI - 1) / kTI) * tiles_h * tiles_w;
   const size_t budget = 227 * 1024 - 1024 - 256;
@@ -423,13 +436,23 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     mk.mark(st);
     count_launch();
   };
+  if (stream) {
+    switch (stages) {
+      case 2: launch(k_conv_tc<T, FN, 2, true>); return;
+      case 3: launch(k_conv_tc<T, FN, 3, true>); return;
+      case 4: launch(k_conv_tc<T, FN, 4, true>); return;
+      default:
+        if (stages >= 5) { launch(k_conv_tc<T, FN, 4, true>); return; }
+        throw Error(Code::Unsupported, "conv_tc: a streamed stage does not fit in shared memory");
+    }
+  }
   switch (stages) {
-    case 1: launch(k_conv_tc<T, FN, 1>); break;
-    case 2: launch(k_conv_tc<T, FN, 2>); break;
-    case 3: launch(k_conv_tc<T, FN, 3>); break;
-    case 4: launch(k_conv_tc<T, FN, 4>); break;
-    case 5: launch(k_conv_tc<T, FN, 5>); break;
-    case 6: launch(k_conv_tc<T, FN, 6>); break;
+    case 1: launch(k_conv_tc<T, FN, 1, false>); break;
+    case 2: launch(k_conv_tc<T, FN, 2, false>); break;
+    case 3: launch(k_conv_tc<T, FN, 3, false>); break;
+    case 4: launch(k_conv_tc<T, FN, 4, false>); break;
+    case 5: launch(k_conv_tc<T, FN, 5, false>); break;
+    case 6: launch(k_conv_tc<T, FN, 6, false>); break;
     default:
       throw Error(Code::Unsupported, "conv_tc: filter bank does not fit in shared memory");
   }
@@ -865,8 +888,12 @@ size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16) {
 
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
   const int es = bf16 ? 2 : 4;
-  return stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8 &&
-         conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256;
+  if (!(stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8)) return false;
+  if (conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256) return true;  // resident bank
+  int FN = 32;
+  while (FN < F) FN *= 2;
+  const size_t a = static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
+  return 2 * (a + static_cast<size_t>(R) * FN * 128) <= 227 * 1024 - 1024 - 256;  // streamed blocks
 }
 
 bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channels through smem

@@ -109,6 +109,8 @@ CONVS = [
     {"kind": "conv2d", "I": [1, 24, 11, 12], "K": [96, 24, 2, 4], "S": 1},    # non-square window
     {"kind": "conv2d", "I": [2, 16, 12, 40], "K": [32, 16, 3, 2], "S": 1},    # S = 2: UMMA N = 64
     {"kind": "conv2d", "I": [1, 48, 10, 70], "K": [128, 48, 3, 1], "S": 1},   # S = 1, F = 128: N = 128
+    {"kind": "conv2d", "I": [3, 128, 14, 18], "K": [128, 128, 3, 3], "S": 1},  # filters streamed per stage
+    {"kind": "conv2d", "I": [2, 96, 11, 13], "K": [100, 96, 3, 3], "S": 1},   # streamed, ragged F / C
 ]
 
 
@@ -157,7 +159,6 @@ GEMM_CONVS = [
     {"kind": "conv2d", "I": [2, 16, 17, 17], "K": [32, 16, 3, 3], "S": 2},
     {"kind": "conv2d", "I": [1, 64, 9, 9], "K": [300, 64, 1, 1], "S": 1},       # F > 256, ragged N tile
     {"kind": "conv2d", "I": [2, 96, 8, 8], "K": [128, 96, 1, 1], "S": 2},      # 1x1 stride-2 projection
-    {"kind": "conv2d", "I": [1, 512, 9, 9], "K": [64, 512, 3, 3], "S": 1},     # large C: weights streamed
 ]
 
 
@@ -165,6 +166,20 @@ GEMM_CONVS = [
 def test_conv_gemm_tf32(doc):
     info = check(doc, "tc_tf32", TF32_TOL)
     assert info["plan"]["family"] == "conv_gemm"
+
+
+# stride-1 windows whose filter bank does not fit in shared memory: conv_tc streams the R filter
+# blocks of each (s, channel chunk) stage next to its A box
+STREAMED = [
+    {"kind": "conv2d", "I": [1, 512, 9, 9], "K": [64, 512, 3, 3], "S": 1},     # large C
+    {"kind": "conv2d", "I": [2, 128, 30, 30], "K": [128, 128, 3, 3], "S": 1},  # ResNet-50 res3 shape
+]
+
+
+@pytest.mark.parametrize("doc", STREAMED, ids=lambda d: json.dumps(d["I"] + d["K"]))
+def test_conv_tc_streamed(doc):
+    info = check(doc, "tc_tf32", TF32_TOL)
+    assert info["plan"]["family"] == "conv_tc", info["plan"]
 
 
 # stride-2 few-channel convs (the ResNet stem) through conv_ns on their space-to-depth form
