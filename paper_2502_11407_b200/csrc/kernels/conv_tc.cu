@@ -63,7 +63,8 @@ template <typename T, int FN, int STAGES, bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
               int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
-              long long* __restrict__ trace) {
+              int G, long long* __restrict__ trace) {
+  // G > 1 (streamed filters only): tile t = (position tile t / G, filter group t % G of FN filters)
   // developer trace (GENSOR_CONV_TRACE=<file>): clock64 marks per CTA, 64 slots
 #define CONV_TRACE(slot, v) \
   if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
@@ -124,9 +125,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long pwait = 0;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int n0 = (t / tiles_img) * kTI;
-        const int h0 = ((t % tiles_img) / tiles_w) * kTH;
-        const int w0 = (t % tiles_w) * kTW;
+        const int tp = t / G, f0 = (t % G) * FN;
+        const int n0 = (tp / tiles_img) * kTI;
+        const int h0 = ((tp % tiles_img) / tiles_w) * kTH;
+        const int w0 = (tp % tiles_w) * kTW;
         for (int ck = 0; ck < nck; ++ck)
           for (int s = 0; s < S; ++s, ++it) {
             const int st = it % STAGES;
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(asm_ + st * stage_bytes, &mapX, &full[st], ck * CK, w0 + s, n0, h0);
             if constexpr (STREAM)
               for (int r = 0; r < R; ++r)
-                tma_load_3d(asm_ + st * stage_bytes + a_bytes + r * W_CHUNK, &mapW, &full[st], ck * CK, 0, r * S + s);
+                tma_load_3d(asm_ + st * stage_bytes + a_bytes + r * W_CHUNK, &mapW, &full[st], ck * CK, f0, r * S + s);
           }
       }
       CONV_TRACE(61, pwait);
@@ -204,13 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int n = (t / tiles_img) * kTI + img;
-      const int h = ((t % tiles_img) / tiles_w) * kTH + hh;
-      const int w = (t % tiles_w) * kTW + wl;
+      const int tp = t / G, f0 = (t % G) * FN;
+      const int n = (tp / tiles_img) * kTI + img;
+      const int h = ((tp % tiles_img) / tiles_w) * kTH + hh;
+      const int w = (tp % tiles_w) * kTW + wl;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
       const bool ok = n < N && h < OH && w < OW;
-      float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
+      float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w + static_cast<int64_t>(f0) * fstride;
 #pragma unroll 1
       for (int c = 0; c < FN; c += 32) {
         uint32_t r[32];
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ok) {
 #pragma unroll
           for (int v = 0; v < 32; ++v)
-            if (c + v < F) __stcs(obase + (c + v) * fstride, __uint_as_float(r[v]));
+            if (f0 + c + v < F) __stcs(obase + (c + v) * fstride, __uint_as_float(r[v]));
         }
       }
       tc_fence_before();
@@ -366,11 +369,12 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
   const size_t a_bytes0 = static_cast<size_t>((kTH + a.R - 1) * kTI * kTW * 128);
   const size_t bank = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
   // resident filter bank when it fits next to two A stages, else filter blocks streamed per stage
-  const bool stream = bank + 2 * a_bytes0 > 227 * 1024 - 1024 - 256;
+  const bool stream = bank + 2 * a_bytes0 > 227 * 1024 - 1024 - 256 || FN < a.F;
+  const int G = (a.F + FN - 1) / FN;  // filter groups (FN < F only with streamed filters)
   const size_t w_bytes = stream ? 0 : bank;
   const size_t a_bytes = a_bytes0 + (stream ? static_cast<size_t>(a.R) * FN * 128 : 0);
   const int tiles_h = (a.OH + kTH - 1) / kTH, tiles_w = (a.OW + kTW - 1) / kTW;
-  const int total = ((a.N + kTI - 1) / kTI) * tiles_h * tiles_w;
+  const int total = ((a.N + kTI - 1) / kTI) * tiles_h * tiles_w * G;
   const size_t budget = 227 * 1024 - 1024 - 256;
   int stages = static_cast<int>((budget - w_bytes) / a_bytes);
   if (stages > 6) stages = 6;
@@ -422,7 +426,7 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
-                                  tiles_w, total, trace),
+                                  tiles_w, total, G, trace),
                "conv_tc launch");
     if (trace) {  // developer path: synchronous dump of the last launch
       std::vector<long long> h(static_cast<size_t>(grid) * 64);
@@ -886,14 +890,19 @@ size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16) {
   return static_cast<size_t>(R) * S * nck * FN * 128 + 2 * static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
 }
 
+bool conv_tc_fits_stream(int R, int FN, bool bf16) {  // two streamed stages fit shared memory
+  (void)bf16;
+  const size_t a = static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
+  return 2 * (a + static_cast<size_t>(R) * FN * 128) <= 227 * 1024 - 1024 - 256;
+}
+
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
   const int es = bf16 ? 2 : 4;
   if (!(stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8)) return false;
   if (conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256) return true;  // resident bank
   int FN = 32;
   while (FN < F) FN *= 2;
-  const size_t a = static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
-  return 2 * (a + static_cast<size_t>(R) * FN * 128) <= 227 * 1024 - 1024 - 256;  // streamed blocks
+  return conv_tc_fits_stream(R, FN, bf16) || conv_tc_fits_stream(R, 128, bf16);  // streamed (split) blocks
 }
 
 bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channels through smem
@@ -929,6 +938,9 @@ void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaSt
   }
   int FN = 32;
   while (FN < a.F) FN *= 2;
+  if (FN > 128 && !conv_tc_fits_stream(a.R, FN, a.bf16) &&
+      conv_tc_smem_need(a.C, a.F, a.R, a.S, a.bf16) > 227 * 1024 - 1024 - 256)
+    FN = 128;  // groups of 128 filters, each a tile of its own
   if (a.bf16) {
     switch (FN) {
       case 32: run_conv<__nv_bfloat16, 32>(a, i, k, o, st, mk); break;

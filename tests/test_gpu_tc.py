@@ -173,6 +173,8 @@ def test_conv_gemm_tf32(doc):
 STREAMED = [
     {"kind": "conv2d", "I": [1, 512, 9, 9], "K": [64, 512, 3, 3], "S": 1},     # large C
     {"kind": "conv2d", "I": [2, 128, 30, 30], "K": [128, 128, 3, 3], "S": 1},  # ResNet-50 res3 shape
+    {"kind": "conv2d", "I": [3, 256, 16, 16], "K": [256, 256, 3, 3], "S": 1},  # F = 256: 2 filter groups
+    {"kind": "conv2d", "I": [2, 64, 12, 12], "K": [200, 64, 3, 3], "S": 1},    # ragged second group
 ]
 
 
