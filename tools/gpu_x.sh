@@ -1,5 +1,6 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sequences.py tests/test_gpu_host_pipe.py -x -q 2>&1 | tail -3 > gpurun_out/pytest_x.log
-timeout 600 python tools/sweep_seq.py resnet50 > gpurun_out/sweep_resnet.log 2>&1
-timeout 900 python bench.py --workload resnet50 --steps 3 --warmup 3 > gpurun_out/bench_resnet50.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_tc.py -x -q -k "conv or s2d" 2>&1 | tail -5 > gpurun_out/pytest_x.log
+L2='{"kind":"conv2d","I":[128,512,9,9],"K":[512,512,3,3],"S":1}'
+python tools/time_op.py "$L2" tc_tf32 10 > gpurun_out/x_l2_tc.log 2>&1
+GENSOR_CONV_FAMILY=gemm python tools/time_op.py "$L2" tc_tf32 10 > gpurun_out/x_l2_gemm.log 2>&1
