@@ -85,6 +85,53 @@ def dist_info():
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def shard_spec(spec: dict, ws: int, rank: int, strong: bool) -> tuple[dict, dict]:
+    """This rank's share of a single-op workload (batch-sharded, no exchange).
+    weak (default): a global batch of ws x the BASELINE batch, one BASELINE-sized shard of
+    distinct images per rank; strong: the BASELINE batch itself split ws ways. The shard axis is
+    the op's outer independent axis (conv/pool images, GEMM batch or rows, GEMV/softmax rows).
+    Returns (this rank's op doc, a description of the global job)."""
+    doc = json.loads(json.dumps(spec["op"]))
+    if doc["kind"] in ("conv2d", "dwconv2d", "avgpool2d"):
+        get = lambda d: d["I"][0]  # noqa: E731
+
+        def put(d, v):
+            d["I"][0] = v
+    elif doc["kind"] == "gemm" and doc.get("batch", 1) > 1:
+        get = lambda d: d["batch"]  # noqa: E731
+
+        def put(d, v):
+            d["batch"] = v
+    else:
+        get = lambda d: d["M"]  # noqa: E731
+
+        def put(d, v):
+            d["M"] = v
+    base = get(doc)
+    if strong:
+        if base % ws:
+            raise SystemExit(f"--strong: the batch {base} does not split {ws} ways")
+        put(doc, base // ws)
+        glob = {"global": base, "per_rank": base // ws, "scaling": "strong"}
+    else:
+        glob = {"global": base * ws, "per_rank": base, "scaling": "weak"}
+    glob["rank_ranges"] = [[r * glob["per_rank"], (r + 1) * glob["per_rank"]] for r in range(ws)]
+    return doc, glob
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under torch.distributed.run
+    with N ranks on 127.0.0.1 (one process per GPU) and relay its output."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
@@ -172,7 +219,7 @@ def tf32_peak(torch, device) -> float:
     return 2 * 8192 ** 3 / best / 1e12
 
 
-def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None, e2e=True, timing=True):
+def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None, e2e=True, timing=True, seed=0):
     """Construct + instantiate + time one op. Returns a dict of measurements (this rank)."""
     op = g.TensorOpSpec.parse_text(json.dumps(spec["op"]))
     cfg = g.EngineConfig(seed=0, mode="b200")
@@ -184,7 +231,7 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
         con.append(time.perf_counter() - t0)
     k = g.Kernel(op, sched, 0, variant)
     rng = torch.Generator(device=device)
-    rng.manual_seed(0)
+    rng.manual_seed(seed)
     xs, out = make_inputs(op, spec, rng, torch, device)
     stream = torch.cuda.current_stream(device)
     for _ in range(warmup):
@@ -268,6 +315,50 @@ def ncu_traffic(workload):
     return None
 
 
+def _pow2(x: int) -> int:
+    p = 1
+    while p < x:
+        p *= 2
+    return p
+
+
+def op_geom(doc: dict) -> dict:
+    """Axes (name, true extent, padded extent), tensor element counts (inputs..., output), and the
+    algorithmic FLOPs / compulsory bytes on true extents of a reference op description — plain
+    Python (op_spec.cpp:70-196 axis orders), so the reference and CPU legs never load the product
+    library."""
+    k, dt, batch = doc["kind"], doc.get("dtype_bytes", 4), doc.get("batch", 1)
+    if k == "gemm":
+        M, K, N = doc["M"], doc["K"], doc["N"]
+        axes, elems = [("m", M), ("n", N), ("k", K)], [M * K, K * N, M * N]
+    elif k in ("gemv", "softmax"):
+        M, N = doc["M"], doc["N"]
+        axes = [("m", M), ("n", N)]
+        elems = [M * N, N, M] if k == "gemv" else [M * N, M * N]
+    else:
+        n, c, h, w = doc["I"]
+        st = doc.get("S", 1)
+        if k == "avgpool2d":
+            r = s_ = doc["F"]
+        else:
+            r, s_ = doc["K"][2], doc["K"][3]
+        oh, ow = (h - r) // st + 1, (w - s_) // st + 1
+        if k == "conv2d":
+            f = doc["K"][0]
+            axes = [("n", n), ("f", f), ("h", oh), ("w", ow), ("c", c), ("r", r), ("s", s_)]
+            elems = [n * c * h * w, f * c * r * s_, n * f * oh * ow]
+        elif k == "dwconv2d":
+            axes = [("n", n), ("c", c), ("h", oh), ("w", ow), ("r", r), ("s", s_)]
+            elems = [n * c * h * w, c * r * s_, n * c * oh * ow]
+        else:
+            axes = [("n", n), ("c", c), ("h", oh), ("w", ow), ("i", r), ("j", s_)]
+            elems = [n * c * h * w, n * c * oh * ow]
+    iters = float(np.prod([float(e) for _, e in axes])) * batch
+    flops = iters if k == "avgpool2d" else (5 * iters if k == "softmax" else 2 * iters)
+    return {"axes": [(a, e, _pow2(e)) for a, e in axes], "elems": [e * batch for e in elems], "flops": flops,
+            "bytes": float(sum(elems)) * dt * batch, "dtype_bytes": dt, "batch": batch}
+
+
 def cpu_baseline(spec, sched_state, budget_s=12.0):
     """The oracle's interpret() of the constructed schedule on a bounded sample, all threads."""
     from oracle import oracle as O
@@ -296,19 +387,16 @@ def cpu_baseline(spec, sched_state, budget_s=12.0):
 
     def run(n):
         d = sized(n)
-        import paper_2502_11407_b200 as g
-
-        op = g.TensorOpSpec.parse_text(json.dumps(d))
+        geo = op_geom(d)
         # the sample shrinks one extent: clamp the schedule's tiles to the sample's padded extents
-        st = {"tiles": [[min(t, a["padded"]) for t in per] for per, a in zip(sched_state["tiles"], op.axes)],
-              "vthreads": [min(v, min(a["padded"], per[-1]) if per else v)
-                           for v, per, a in zip(sched_state["vthreads"], sched_state["tiles"], op.axes)]}
+        st = {"tiles": [[min(t, a[2]) for t in per] for per, a in zip(sched_state["tiles"], geo["axes"])],
+              "vthreads": [min(v, min(a[2], per[-1]) if per else v)
+                           for v, per, a in zip(sched_state["vthreads"], sched_state["tiles"], geo["axes"])]}
         rng = np.random.default_rng(0)
-        xs = [rng.uniform(-1, 1, int(np.prod(t["true_dims"])) * op.batch).astype(np.float32)
-              for t in op.tensors[:-1]]
+        xs = [rng.uniform(-1, 1, e).astype(np.float32) for e in geo["elems"][:-1]]
         t0 = time.perf_counter()
         O.interpret(d, st, xs, threads=threads)
-        return time.perf_counter() - t0, op.flops, op.bytes
+        return time.perf_counter() - t0, geo["flops"], geo["bytes"]
 
     n = 1
     dt, fl, by = run(n)
@@ -339,20 +427,16 @@ def run_reference(args):
     if rank != 0:
         return
     spec = WORKLOADS[args.workload]
-    from oracle import oracle as O, ref
-
-    import paper_2502_11407_b200 as g
+    from oracle import ref  # the reference's own construct library; never the product package
 
     op_doc = spec["op"]
     if ref.available():
         con = ref.optimize(op_doc, B200_REF_HW, {"seed": 0})
         state = con["results"][0]["state"]
         construct_kind = "reference (oracle/_ref: unmodified proj/src)"
-    else:  # reference sources absent on this box: same schedule from the bit-identical port
-        op = g.TensorOpSpec.parse_text(json.dumps(op_doc))
-        hw = g.HardwareSpec.load_text(json.dumps(B200_REF_HW))
-        state = g.optimize(op, hw, g.EngineConfig(seed=0))[0]["state"]
-        construct_kind = "port (reference-compatible engine, bit-identical)"
+    else:  # reference library absent: the schedule-independent naive loop nest (level-less state)
+        state = {"tiles": [[] for _ in op_geom(op_doc)["axes"]], "vthreads": [1] * len(op_geom(op_doc)["axes"])}
+        construct_kind = "none (oracle/_ref not built): interpret() of the unscheduled loop nest"
     base = cpu_baseline(spec, state, budget_s=args.ref_budget)
     times = []
     for _ in range(args.warmup + args.steps):
@@ -677,11 +761,13 @@ def run_ours(args):
             pg.destroy_process_group()
         return
 
-    spec = WORKLOADS[args.workload]
+    # this rank's batch shard (weak by default: a BASELINE-sized shard of distinct images per rank)
+    doc, glob = shard_spec(WORKLOADS[args.workload], ws, rank, args.strong)
+    spec = dict(WORKLOADS[args.workload], op=doc)
 
     barrier()
     with ClockSampler(local) as clk:
-        res = run_op(g, torch, spec, hw, args.steps, args.warmup, device, args.variant, flush)
+        res = run_op(g, torch, spec, hw, args.steps, args.warmup, device, args.variant, flush, seed=rank)
     barrier()
     total_ms = sum(res["step_ms"])
     e2e_ms = statistics.mean(res["e2e_ms"])
@@ -734,7 +820,7 @@ def run_ours(args):
         return
     line = {
         "metric": METRIC, "value": value, "unit": spec["unit"], "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": glob["scaling"],
         "vs_baseline": None,
         "dtype": {"tc_tf32": "tf32 (fp32 storage, fp32 accumulate)", "tc_bf16": "bf16 (fp32 accumulate)",
                   "simt_f32": "f32", "simt_parity": "f64 accumulate", "stream": "f32"}[info["variant_name"]],
@@ -742,7 +828,10 @@ def run_ours(args):
         "config": {"workload": spec["name"], "op": spec["op"], "variant": info["variant_name"],
                    "schedule": info["state"]["repr"], "kernel_plan": info["plan"], "engine": "b200 mode",
                    "l2": "flushed between steps (256 MiB write outside the events)",
-                   "parallelism": f"weak: {ws} independent replica(s), one per GPU (batch-sharded layer), no collective"},
+                   "batch": glob,
+                   "parallelism": (f"{glob['scaling']}: global batch {glob['global']} sharded {glob['per_rank']} per rank "
+                                   f"over {ws} GPU(s) (distinct synthetic data per rank), one process per GPU, "
+                                   "no collective on the compute path")},
         "roofline": rl,
         "e2e": {"value": e2e_value, "unit": spec["unit"], "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
@@ -760,6 +849,50 @@ def run_ours(args):
         pg.destroy_process_group()
 
 
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): every rank derives its shard of the
+    workload, runs `steps` timed host-side placeholder steps (a sleep proportional to its shard
+    and rank, standing in for the device work), and the timed region goes through the same
+    barrier + max-over-ranks reduction as the real run. Tests drive it with --gpus 2."""
+    import torch
+
+    ws, rank, _ = dist_info()
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        pg = dist
+    spec = WORKLOADS[args.workload]
+    doc, glob = shard_spec(spec, ws, rank, args.strong)
+    geo = op_geom(doc)
+    if pg:
+        pg.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.002 * (rank + 1))
+    ms = (time.perf_counter() - t0) * 1e3
+    if pg:
+        pg.barrier()
+    per_rank = [None] * ws
+    t = torch.tensor([ms], dtype=torch.float64)
+    if pg:
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        pg.all_gather_object(per_rank, {"rank": rank, "op": doc, "ms": ms, "flops": geo["flops"]})
+    else:
+        per_rank = [{"rank": 0, "op": doc, "ms": ms, "flops": geo["flops"]}]
+    if rank == 0:
+        total = t.item()
+        flops = sum(r["flops"] for r in per_rank)
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": flops / (total / args.steps / 1e3) / 1e12,
+                          "unit": "TFLOP/s (placeholder timing)", "n_gpus": ws, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": total / args.steps, "scaling": glob["scaling"],
+                          "config": {"workload": spec["name"], "batch": glob, "backend": "gloo" if pg else None},
+                          "ranks": per_rank}), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -771,10 +904,18 @@ def main():
     ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: split the BASELINE batch N ways (default: one BASELINE-sized shard per rank)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: exercise the rank plumbing (gloo) and the sharding; no kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -9,8 +9,10 @@
  *   - gensor_last_error() returns a thread-local "<CodeName>: detail" message, the reference's
  *     what() text (error.hpp:33-34);
  *   - op / hw / schedule handles are opaque and immutable after creation, safe to share across
- *     threads; a kernel handle runs one execute at a time (per-handle device workspace), so use
- *     one kernel handle per concurrent stream;
+ *     threads; a kernel handle's plan is immutable too: gensor_execute may be called on one
+ *     handle from several threads and streams at once (each stream gets its own device
+ *     workspace; gensor_execute_ws takes a caller-owned one). gensor_execute_host and the timing
+ *     instrumentation take a non-const handle and run one call at a time;
  *   - lifetimes: an op must outlive every schedule and kernel made from it (the reference's
  *     ETIRState keeps a non-owning op pointer, etir.hpp:75); a hw must outlive schedules;
  *   - JSON outputs use caller buffers: on cap < need the call returns GENSOR_ETRUNCATED and
@@ -168,6 +170,14 @@ int gensor_kernel_info(const gensor_kernel* k, char* buf, size_t cap, size_t* ne
  * layouts (op_spec.cpp:251-262). fp32 tensors for dtype_bytes 4, bf16 for dtype_bytes 2. */
 int gensor_execute(const gensor_kernel* k, const void* const* d_inputs, int n_inputs, void* d_output,
                    void* stream);
+/* Device workspace one execute needs (bytes; 0 for families without a pre-pass). */
+int gensor_kernel_workspace_size(const gensor_kernel* k, size_t* bytes);
+/* gensor_execute with a caller-owned device workspace of at least gensor_kernel_workspace_size
+ * bytes (the cuDNN/cuBLASLt convention): concurrent calls on one handle with distinct workspaces
+ * never touch shared device state. gensor_execute uses a per-stream workspace owned by the handle
+ * (allocated on the stream's first execute). */
+int gensor_execute_ws(const gensor_kernel* k, const void* const* d_inputs, int n_inputs, void* d_output,
+                      void* d_workspace, size_t workspace_bytes, void* stream);
 /* Host-buffer execute, the interpreter's calling convention: copies the inputs host->device,
  * runs, copies the output back and synchronises. Device staging buffers are owned by the
  * kernel handle (one call at a time per handle). */

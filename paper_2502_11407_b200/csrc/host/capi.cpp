@@ -90,6 +90,15 @@ int guarded(F&& f) {
   }
 }
 
+// A kernel is instantiated from a schedule of the SAME operator: the schedule's tiles index that
+// op's axes and padded extents (an ETIRState belongs to one TensorOpSpec, etir.hpp:75).
+void check_schedule_op(const gb::OpDesc& op, const gensor_schedule& s) {
+  if (s.op == &op) return;
+  if (!s.op || s.op->to_json() != op.to_json())
+    throw gb::Error(gb::Code::ShapeMismatch, "schedule was constructed for " + (s.op ? s.op->label() : std::string("?")) +
+                                                 ", not for " + op.label());
+}
+
 int emit(const std::string& s, char* buf, size_t cap, size_t* need) {
   if (need) *need = s.size() + 1;
   if (!buf || cap < s.size() + 1) return fail(GENSOR_ETRUNCATED, "output buffer too small");
@@ -434,6 +443,7 @@ int gensor_kernel_prepare(const gensor_op* op, const gensor_schedule* s, int ind
   return guarded([&]() -> int {
     if (index < 0 || index >= static_cast<int>(s->results.size()))
       return fail(GENSOR_EINVALID, "schedule index out of range");
+    check_schedule_op(op->op, *s);
     const gb::Sched& st = s->results[static_cast<size_t>(index)].state;
     if (!st.complete()) throw gb::Error(gb::Code::IncompleteState, "kernel needs a complete schedule");
     auto* k = new gensor_kernel;
@@ -456,7 +466,23 @@ int gensor_kernel_info(const gensor_kernel* k, char* buf, size_t cap, size_t* ne
 int gensor_execute(const gensor_kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream) {
   if (!k || !d_out || (n_in > 0 && !d_in)) return fail(GENSOR_EINVALID, "null argument");
   return guarded([&]() -> int {
-    gb::dev::execute(k->k, d_in, n_in, d_out, stream);
+    gb::dev::execute(k->k, d_in, n_in, d_out, nullptr, 0, stream);
+    return GENSOR_OK;
+  });
+}
+
+int gensor_kernel_workspace_size(const gensor_kernel* k, size_t* bytes) {
+  if (!k || !bytes) return fail(GENSOR_EINVALID, "null argument");
+  *bytes = gb::dev::workspace_bytes(k->k);
+  return GENSOR_OK;
+}
+
+int gensor_execute_ws(const gensor_kernel* k, const void* const* d_in, int n_in, void* d_out, void* d_workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!k || !d_out || (n_in > 0 && !d_in)) return fail(GENSOR_EINVALID, "null argument");
+  if (gb::dev::workspace_bytes(k->k) > 0 && !d_workspace) return fail(GENSOR_EINVALID, "null workspace");
+  return guarded([&]() -> int {
+    gb::dev::execute(k->k, d_in, n_in, d_out, d_workspace, workspace_bytes, stream);
     return GENSOR_OK;
   });
 }
@@ -473,6 +499,7 @@ int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, co
                   void* d_out, void* stream, int iters, char* buf, size_t cap, size_t* need) {
   if (!op || !s || !d_out || (n_in > 0 && !d_in)) return fail(GENSOR_EINVALID, "null argument");
   return guarded([&]() -> int {
+    check_schedule_op(op->op, *s);
     std::vector<std::pair<float, int>> t;
     std::ostringstream os;
     os << "{\"ms\":[";

@@ -84,6 +84,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     // producer warp (group g, index pw): MN chunk pw (positions 32*pw .. 32*pw+31 of the tile),
     // all 32 channels of the k-block; lane = position. Group 0 additionally issues the B TMA.
     const int grp = warp >> 2, pw = warp & 3;
+    // the B-issuing lanes read W', which the preceding pre-pass launch writes (programmatic
+    // dependent launch: this grid may start before it completes)
+    if (pw == 0 && lane == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int mt = t / tiles_n, nt = t % tiles_n;
@@ -258,18 +261,18 @@ __global__ void __launch_bounds__(256) k_filters_rsfc(const float* __restrict__ 
 }
 
 template <int BN>
-void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
+constexpr int conv_gemm_stages() {
   constexpr size_t STAGE = 128 * 128 + BN * 128;
-  constexpr int STAGES = static_cast<int>((227 * 1024 - 2048 - 16384) / STAGE) >= 4 ? 4 : 3;
+  return static_cast<int>((227 * 1024 - 2048 - 16384) / STAGE) >= 4 ? 4 : 3;
+}
+
+template <int BN>
+void run_gemm_conv(const ConvGemmArgs& a, const CUtensorMap& mapW, const float* I, const float* K, float* O, void* ws,
+                   cudaStream_t st, Marks& mk) {
+  constexpr size_t STAGE = 128 * 128 + BN * 128;
+  constexpr int STAGES = conv_gemm_stages<BN>();
   const int Cp = a.packed ? (a.S * a.C + 3) / 4 * 4 : (a.C + 3) / 4 * 4;
   const int planes = a.packed ? a.R : a.R * a.S;
-  if (!a.map_ready) {
-    const uint64_t dw[3] = {static_cast<uint64_t>(Cp), static_cast<uint64_t>(a.F), static_cast<uint64_t>(planes)};
-    const uint64_t sw[2] = {static_cast<uint64_t>(Cp) * 4, static_cast<uint64_t>(Cp) * a.F * 4};
-    const uint32_t bw[3] = {32, static_cast<uint32_t>(BN), 1};
-    encode_map(&a.mapW, false, true, a.ws_w, 3, dw, sw, bw);
-    a.map_ready = true;
-  }
   const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
   const int tiles_m = static_cast<int>((P + 127) / 128), tiles_n = (a.F + BN - 1) / BN;
   const int total = tiles_m * tiles_n;
@@ -277,7 +280,7 @@ void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cu
   mk.mark(st);
   const int64_t wt = static_cast<int64_t>(a.F) * Cp * planes;
   k_filters_rsfc<<<static_cast<unsigned>(std::min<int64_t>(4 * a.sms, (wt + 255) / 256)), 256, 0, st>>>(
-      K, static_cast<float*>(a.ws_w), a.F, a.C, Cp, a.R * a.S, a.S, a.packed);
+      K, static_cast<float*>(ws), a.F, a.C, Cp, a.R * a.S, a.S, a.packed);
   check_cuda(cudaGetLastError(), "filters_rsfc launch");
   count_launch();
   auto kern = k_conv_gemm<BN, STAGES>;
@@ -294,7 +297,7 @@ void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cu
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  check_cuda(cudaLaunchKernelEx(&cfg, kern, I, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.stride, a.OH, a.OW,
+  check_cuda(cudaLaunchKernelEx(&cfg, kern, I, mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.stride, a.OH, a.OW,
                                 tiles_m, tiles_n, total, a.packed),
              "conv_gemm launch");
   count_launch();
@@ -303,14 +306,24 @@ void run_gemm_conv(ConvGemmArgs& a, const float* I, const float* K, float* O, cu
 
 }  // namespace
 
-void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {
+void conv_gemm_map(const ConvGemmArgs& a, void* ws, CUtensorMap& mapW) {
+  const int Cp = a.packed ? (a.S * a.C + 3) / 4 * 4 : (a.C + 3) / 4 * 4;
+  const int planes = a.packed ? a.R : a.R * a.S;
+  const uint64_t dw[3] = {static_cast<uint64_t>(Cp), static_cast<uint64_t>(a.F), static_cast<uint64_t>(planes)};
+  const uint64_t sw[2] = {static_cast<uint64_t>(Cp) * 4, static_cast<uint64_t>(Cp) * a.F * 4};
+  const uint32_t bw[3] = {32, static_cast<uint32_t>(a.BN), 1};
+  encode_map(&mapW, false, true, ws, 3, dw, sw, bw);
+}
+
+void launch_conv_gemm(const ConvGemmArgs& a, const CUtensorMap& mapW, const void* I, const void* K, void* O, void* ws,
+                      cudaStream_t st, Marks& mk) {
   const float* i = static_cast<const float*>(I);
   const float* k = static_cast<const float*>(K);
   float* o = static_cast<float*>(O);
   switch (a.BN) {
-    case 64: run_gemm_conv<64>(a, i, k, o, st, mk); break;
-    case 128: run_gemm_conv<128>(a, i, k, o, st, mk); break;
-    default: run_gemm_conv<256>(a, i, k, o, st, mk); break;
+    case 64: run_gemm_conv<64>(a, mapW, i, k, o, ws, st, mk); break;
+    case 128: run_gemm_conv<128>(a, mapW, i, k, o, ws, st, mk); break;
+    default: run_gemm_conv<256>(a, mapW, i, k, o, ws, st, mk); break;
   }
 }
 

@@ -24,10 +24,8 @@
 //   * 4 epilogue warps: tcgen05.ld -> streaming stores into NCHW.
 #include <cuda_bf16.h>
 
-#include <cstdio>
-#include <cstdlib>
+#include <algorithm>
 #include <type_traits>
-#include <vector>
 
 #include "../host/error.hpp"
 #include "common.cuh"
@@ -63,11 +61,8 @@ template <typename T, int FN, int STAGES, bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW, float* __restrict__ O, int N,
               int C, int H, int W, int F, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
-              int G, long long* __restrict__ trace) {
+              int G) {
   // G > 1 (streamed filters only): tile t = (position tile t / G, filter group t % G of FN filters)
-  // developer trace (GENSOR_CONV_TRACE=<file>): clock64 marks per CTA, 64 slots
-#define CONV_TRACE(slot, v) \
-  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int CK = 128 / sizeof(T);        // channels per 128 B row
   constexpr uint32_t W_CHUNK = FN * 128;     // one (r, s, c-chunk) slice of W'
   constexpr uint32_t IDESC = instr_desc(ConvTraits<T>::kFormat, 128, FN, 0, 0);
@@ -122,7 +117,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
       tma_prefetch(&mapX);
       if constexpr (STREAM) tma_prefetch(&mapW);
-      long long pwait = 0;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int tp = t / G, f0 = (t % G) * FN;
@@ -132,9 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ck = 0; ck < nck; ++ck)
           for (int s = 0; s < S; ++s, ++it) {
             const int st = it % STAGES;
-            const long long tw0 = trace ? clock64() : 0;
             mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-            if (trace) pwait += clock64() - tw0;
             mbar_arrive_expect_tx(&full[st], stage_bytes);
             tma_load_4d(asm_ + st * stage_bytes, &mapX, &full[st], ck * CK, w0 + s, n0, h0);
             if constexpr (STREAM)
@@ -142,11 +134,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_3d(asm_ + st * stage_bytes + a_bytes + r * W_CHUNK, &mapW, &full[st], ck * CK, f0, r * S + s);
           }
       }
-      CONV_TRACE(61, pwait);
     }
   } else if (warp == kMmaWarp) {
     if (elect_one()) {
-      CONV_TRACE(0, clock64());
       // W' is written by the preceding conversion launch (programmatic dependent launch: this
       // grid starts early and only this thread waits for the primary grid's results)
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -157,24 +147,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ck = 0; ck < nck; ++ck) tma_load_3d(wsm + (rs * nck + ck) * W_CHUNK, &mapW, wbar, ck * CK, 0, rs);
         mbar_wait(wbar, 0);
       }
-      CONV_TRACE(2, clock64());
-      long long fwait = 0;
       const uint32_t w_addr = smem_u32(wsm);
       const uint32_t a_base = smem_u32(asm_);
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
-        if (local < 4) CONV_TRACE(3 + 2 * local, clock64());
         tc_fence_after();
         const uint32_t d = tmem + acc * FN;
         bool first = true;
         for (int ck = 0; ck < nck; ++ck)
           for (int s = 0; s < S; ++s, ++it) {
             const int st = it % STAGES;
-            const long long tw0 = trace ? clock64() : 0;
             mbar_wait(&full[st], (it / STAGES) & 1);
-            if (trace) fwait += clock64() - tw0;
             tc_fence_after();
             const uint32_t a_addr = a_base + st * stage_bytes;
             for (int r = 0; r < R; ++r) {
@@ -193,9 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit(&empty[st]);
           }
         mma_commit(&acc_full[acc]);
-        if (local < 4) CONV_TRACE(4 + 2 * local, clock64());
       }
-      CONV_TRACE(60, fwait);
     }
   } else {
     // ---- epilogue warps: drain TMEM into NCHW ----
@@ -228,7 +211,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      if (warp == kMmaWarp + 1 && lane == 0 && local < 4) CONV_TRACE(40 + local, clock64());
     }
   }
   tc_fence_before();
@@ -246,13 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kBandRows = 2;  // pre-pass: max input rows per block (shared-memory sizing)
 
 // rows per pre-pass block: 2 (measured: 1-row bands 10.7 us, 2-row 9.2 us for C; 464 B runs per
-// channel), GENSOR_PREPASS_BAND=1..4 for developer A/B
-int prepass_band(int W) {
-  static const int env = std::getenv("GENSOR_PREPASS_BAND") ? std::atoi(std::getenv("GENSOR_PREPASS_BAND")) : 0;
-  if (env >= 1 && env <= 4) return env;
-  (void)W;
-  return 2;
-}
+// channel)
+constexpr int kPrepassBand = 2;
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ I, const float* __restrict__ K,
@@ -362,59 +339,81 @@ __global__ void __launch_bounds__(256) k_conv_prepass(const float* __restrict__ 
   }
 }
 
-template <typename T, int FN>
-void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
-  constexpr int CK = 128 / sizeof(T);
+// conv_tc geometry shared by the map builder and the launch: filters per tile group (FN),
+// whether the filter bank streams per stage, the stage count.
+bool tc_fits_stream(int R, int FN) {  // two streamed stages fit shared memory
+  const size_t a = static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
+  return 2 * (a + static_cast<size_t>(R) * FN * 128) <= 227 * 1024 - 1024 - 256;
+}
+
+struct TcGeom {
+  int FN = 32, G = 1, stages = 0, tiles_h = 0, tiles_w = 0, total = 0;
+  bool stream = false;
+  size_t w_bytes = 0, a_bytes = 0;
+};
+
+TcGeom tc_geom(const ConvTcArgs& a) {
+  TcGeom g;
+  while (g.FN < a.F) g.FN *= 2;
+  if (g.FN > 128 && !tc_fits_stream(a.R, g.FN) &&
+      conv_tc_smem_need(a.C, a.F, a.R, a.S, a.bf16) > 227 * 1024 - 1024 - 256)
+    g.FN = 128;  // groups of 128 filters, each a tile of its own
+  const int CK = a.bf16 ? 64 : 32;
   const int nck = (a.C + CK - 1) / CK;
   const size_t a_bytes0 = static_cast<size_t>((kTH + a.R - 1) * kTI * kTW * 128);
-  const size_t bank = static_cast<size_t>(a.R * a.S * nck) * FN * 128;
+  const size_t bank = static_cast<size_t>(a.R * a.S * nck) * g.FN * 128;
   // resident filter bank when it fits next to two A stages, else filter blocks streamed per stage
-  const bool stream = bank + 2 * a_bytes0 > 227 * 1024 - 1024 - 256 || FN < a.F;
-  const int G = (a.F + FN - 1) / FN;  // filter groups (FN < F only with streamed filters)
-  const size_t w_bytes = stream ? 0 : bank;
-  const size_t a_bytes = a_bytes0 + (stream ? static_cast<size_t>(a.R) * FN * 128 : 0);
-  const int tiles_h = (a.OH + kTH - 1) / kTH, tiles_w = (a.OW + kTW - 1) / kTW;
-  const int total = ((a.N + kTI - 1) / kTI) * tiles_h * tiles_w * G;
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  int stages = static_cast<int>((budget - w_bytes) / a_bytes);
-  if (stages > 6) stages = 6;
-  const int grid = std::min(total, a.sms);
-  if (!a.maps_ready) {
-    const int es = sizeof(T);
-    const uint64_t dw[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.F),
-                            static_cast<uint64_t>(a.R) * a.S};
-    const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.C) * a.F * es};
-    const uint32_t bw[3] = {static_cast<uint32_t>(CK), static_cast<uint32_t>(FN), 1};
-    encode_map(&a.mapW, es == 2, es == 4, a.ws_w, 3, dw, sw, bw);
-    // NHWC copy viewed as (c, w, n, h): box {CK, 8, 2, 8+R-1} -> smem rows h*16 + img*8 + w
-    const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.N),
-                            static_cast<uint64_t>(a.H)};
-    const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.H) * a.W * a.C * es,
-                            static_cast<uint64_t>(a.W) * a.C * es};
-    const uint32_t bx[4] = {static_cast<uint32_t>(CK), kTW, kTI, static_cast<uint32_t>(kTH + a.R - 1)};
-    encode_map(&a.mapX, es == 2, es == 4, a.ws_x, 4, dx, sx, bx);
-    a.maps_ready = true;
-  }
+  g.stream = bank + 2 * a_bytes0 > 227 * 1024 - 1024 - 256 || g.FN < a.F;
+  g.G = (a.F + g.FN - 1) / g.FN;  // filter groups (FN < F only with streamed filters)
+  g.w_bytes = g.stream ? 0 : bank;
+  g.a_bytes = a_bytes0 + (g.stream ? static_cast<size_t>(a.R) * g.FN * 128 : 0);
+  g.tiles_h = (a.OH + kTH - 1) / kTH;
+  g.tiles_w = (a.OW + kTW - 1) / kTW;
+  g.total = ((a.N + kTI - 1) / kTI) * g.tiles_h * g.tiles_w * g.G;
+  g.stages = static_cast<int>((227 * 1024 - 1024 - 256 - g.w_bytes) / g.a_bytes);
+  if (g.stages > 6) g.stages = 6;
+  return g;
+}
+
+void tc_maps(const ConvTcArgs& a, void* ws, ConvTcMaps& m) {
+  const TcGeom g = tc_geom(a);
+  const int es = a.bf16 ? 2 : 4, CK = 128 / es;
+  const uint64_t dw[3] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.F), static_cast<uint64_t>(a.R) * a.S};
+  const uint64_t sw[2] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.C) * a.F * es};
+  const uint32_t bw[3] = {static_cast<uint32_t>(CK), static_cast<uint32_t>(g.FN), 1};
+  encode_map(&m.W, es == 2, es == 4, static_cast<char*>(ws) + a.w_off, 3, dw, sw, bw);
+  // NHWC copy viewed as (c, w, n, h): box {CK, 8, 2, 8+R-1} -> smem rows h*16 + img*8 + w
+  const uint64_t dx[4] = {static_cast<uint64_t>(a.C), static_cast<uint64_t>(a.W), static_cast<uint64_t>(a.N),
+                          static_cast<uint64_t>(a.H)};
+  const uint64_t sx[3] = {static_cast<uint64_t>(a.C) * es, static_cast<uint64_t>(a.H) * a.W * a.C * es,
+                          static_cast<uint64_t>(a.W) * a.C * es};
+  const uint32_t bx[4] = {static_cast<uint32_t>(CK), kTW, kTI, static_cast<uint32_t>(kTH + a.R - 1)};
+  encode_map(&m.X, es == 2, es == 4, static_cast<char*>(ws) + a.x_off, 4, dx, sx, bx);
+}
+
+template <typename T, int FN>
+void run_conv(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const float* K, float* O, void* ws,
+              cudaStream_t st, Marks& mk) {
+  const TcGeom g = tc_geom(a);
+  const int grid = std::min(g.total, a.sms);
+  T* ws_w = reinterpret_cast<T*>(static_cast<char*>(ws) + a.w_off);
+  T* ws_x = reinterpret_cast<T*>(static_cast<char*>(ws) + a.x_off);
   auto launch = [&](auto kern) {
-    const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + 256;
+    const size_t smem = g.w_bytes + static_cast<size_t>(g.stages) * g.a_bytes + 1024 + 256;
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_tc smem attribute");
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    const int band = prepass_band(a.W);
+    const int band = kPrepassBand;
     const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
     check_cuda(cudaFuncSetAttribute(k_conv_prepass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(pre_smem)),
                "prepass smem attribute");
-    k_conv_prepass<T><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(I, K, static_cast<T*>(a.ws_x),
-                                                                 static_cast<T*>(a.ws_w), a.N, a.C, a.H, a.W, a.F,
-                                                                 a.R * a.S, band);
+    k_conv_prepass<T><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(I, K, ws_x, ws_w, a.N, a.C,
+                                                                                         a.H, a.W, a.F, a.R * a.S, band);
     check_cuda(cudaGetLastError(), "conv prepass launch");
     count_launch();
-    static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
-    static long long* trace = nullptr;
-    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -425,32 +424,23 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, tiles_h,
-                                  tiles_w, total, G, trace),
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, m.X, m.W, O, a.N, a.C, a.H, a.W, a.F, a.R, a.S, a.OH, a.OW, g.tiles_h,
+                                  g.tiles_w, g.total, g.G),
                "conv_tc launch");
-    if (trace) {  // developer path: synchronous dump of the last launch
-      std::vector<long long> h(static_cast<size_t>(grid) * 64);
-      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
-      if (FILE* f = std::fopen(trace_path, "w")) {
-        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
-        std::fclose(f);
-      }
-    }
-    check_cuda(cudaGetLastError(), "conv_tc launch");
     mk.mark(st);
     count_launch();
   };
-  if (stream) {
-    switch (stages) {
+  if (g.stream) {
+    switch (g.stages) {
       case 2: launch(k_conv_tc<T, FN, 2, true>); return;
       case 3: launch(k_conv_tc<T, FN, 3, true>); return;
       case 4: launch(k_conv_tc<T, FN, 4, true>); return;
       default:
-        if (stages >= 5) { launch(k_conv_tc<T, FN, 4, true>); return; }
+        if (g.stages >= 5) { launch(k_conv_tc<T, FN, 4, true>); return; }
         throw Error(Code::Unsupported, "conv_tc: a streamed stage does not fit in shared memory");
     }
   }
-  switch (stages) {
+  switch (g.stages) {
     case 1: launch(k_conv_tc<T, FN, 1, false>); break;
     case 2: launch(k_conv_tc<T, FN, 2, false>); break;
     case 3: launch(k_conv_tc<T, FN, 3, false>); break;
@@ -461,7 +451,6 @@ void run_conv(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStrea
       throw Error(Code::Unsupported, "conv_tc: filter bank does not fit in shared memory");
   }
 }
-
 
 // Space-to-depth pre-pass for stride-2 convs with few channels (the ResNet stem): blocks
 // [0, xblocks) write X2[n][h2][w2][(c, dy, dx)] = I[n][c][2 h2 + dy][2 w2 + dx] (0 outside), the
@@ -541,7 +530,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     k_conv_ns(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapO, int tma_store, float* __restrict__ O, int N,
               int C, int H, int W, int F, int FN, int R, int S, int OH, int OW, int tiles_h, int tiles_w, int total,
-              int valid_w, long long* __restrict__ trace) {
+              int valid_w) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nck = (C + 31) / 32;
@@ -561,8 +550,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   float* stage_o = reinterpret_cast<float*>(smem + w_bytes + STAGES * a_bytes + 1024);  // [8 warps][8][32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_img = tiles_h * tiles_w;
-#define NS_TRACE(slot, v) \
-  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
   constexpr int kMma = 1;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -592,7 +579,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     if (elect_one()) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
       tma_prefetch(&mapX);
-      long long pwait = 0;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int n = t / tiles_img;
@@ -600,20 +586,15 @@ __global__ void __launch_bounds__(kNsThreads, 1)
         const int w0 = (t % tiles_w) * valid_w;
         for (int ck = 0; ck < nck; ++ck, ++it) {
           const int st = it % STAGES;
-          const long long tw0 = trace ? clock64() : 0;
           mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
-          if (trace) pwait += clock64() - tw0;
           mbar_arrive_expect_tx(&full[st], a_bytes);
           tma_load_4d(asm_ + st * a_bytes, &mapX, &full[st], ck * 32, w0, h0, n);
         }
       }
-      NS_TRACE(61, pwait);
     }
   } else if (warp == kMma) {
     if (elect_one()) {
-      NS_TRACE(0, clock64());
       asm volatile("griddepcontrol.wait;" ::: "memory");  // W' is written by the preceding launch
-      NS_TRACE(1, clock64());
       tma_prefetch(&mapW);
       // chunk-major filter loads with a barrier per chunk: the first chunk's MMAs start once its
       // R*S blocks have landed instead of after the whole bank
@@ -626,23 +607,18 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           for (int s = 0; s < S; ++s)
             tma_load_3d(wsm + ((r * nck + ck) * S + s) * FN * 128, &mapW, wb, ck * 32, 0, r * S + s);
       }
-      NS_TRACE(2, clock64());
-      long long fwait = 0;
       const uint32_t idesc = instr_desc(2, 128, static_cast<uint32_t>(ncol), 0, 0);
       const uint32_t w_addr = smem_u32(wsm), a_base = smem_u32(asm_);
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
-        if (local < 4) NS_TRACE(3 + 2 * local, clock64());
         tc_fence_after();
         const uint32_t d = tmem + acc * ncol;
         bool first = true;
         for (int ck = 0; ck < nck; ++ck, ++it) {
           const int st = it % STAGES;
-          const long long tw0 = trace ? clock64() : 0;
           mbar_wait(&full[st], (it / STAGES) & 1);
-          if (trace) fwait += clock64() - tw0;
           if (local == 0 && ck < kWb) mbar_wait(&wbar[ck], 0);  // chunk ck's filters (last: the rest)
           tc_fence_after();
           const uint32_t a_addr = a_base + st * a_bytes;
@@ -659,9 +635,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           mma_commit(&empty[st]);
         }
         mma_commit(&acc_full[acc]);
-        if (local < 4) NS_TRACE(4 + 2 * local, clock64());
       }
-      NS_TRACE(60, fwait);
     }
   } else {
     // ---- epilogue: warp q owns TMEM lanes 32q.. = tile row q; lane = input column w0 + lane.
@@ -675,7 +649,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const int h = ((t % tiles_img) / tiles_w) * kNsRows + q;
       const int w = (t % tiles_w) * valid_w + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
-      if (warp == kMma + 1 && lane == 0 && local < 4) NS_TRACE(44 + local, clock64());
       tc_fence_after();
       const bool ok = lane < valid_w && n < N && h < OH && w < OW;
       float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
@@ -748,7 +721,6 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           }
         }
       }
-      if (warp == kMma + 1 && lane == 0 && local < 4) NS_TRACE(40 + local, clock64());
     }
     if (tma_store && lane == 0) bulk_wait<0>();  // output stores complete before the CTA retires
   }
@@ -761,76 +733,94 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   }
 }
 
-void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaStream_t st, Marks& mk) {
-  int FN = 32;
-  while (FN < a.F) FN *= 2;
-  // the kernel's problem: the op itself, or (stride 2) its space-to-depth form — a stride-1 conv
-  // over C2 = 4C channels (c, dy, dx) of ceil(H/2) x ceil(W/2) positions with ceil(R/2) x
-  // ceil(S/2) filters (K'[f][(c,dy,dx)][r'][s'] = K[f][c][2r'+dy][2s'+dx], 0 past the window)
-  const int gC = a.s2d ? 4 * a.C : a.C, gH = a.s2d ? (a.H + 1) / 2 : a.H, gW = a.s2d ? (a.W + 1) / 2 : a.W;
-  const int gR = a.s2d ? (a.R + 1) / 2 : a.R, gS = a.s2d ? (a.S + 1) / 2 : a.S;
-  const int nck = (gC + 31) / 32;
-  const size_t w_bytes = static_cast<size_t>(gR) * nck * gS * FN * 128;
-  const size_t a_bytes = static_cast<size_t>(kNsRows + gR - 1) * 4096;
+// conv_ns geometry: the kernel's problem is the op itself, or (stride 2) its space-to-depth form —
+// a stride-1 conv over C2 = 4C channels (c, dy, dx) of ceil(H/2) x ceil(W/2) positions with
+// ceil(R/2) x ceil(S/2) filters (K'[f][(c,dy,dx)][r'][s'] = K[f][c][2r'+dy][2s'+dx], 0 past the window)
+struct NsGeom {
+  int FN = 32, gC = 0, gH = 0, gW = 0, gR = 0, gS = 0, nck = 0;
+  int valid_w = 0, tiles_w = 0, tiles_h = 0, total = 0, stages = 0;
+  bool tma_store = false;
+  size_t w_bytes = 0, a_bytes = 0, stage_o = 0;
+};
+
+NsGeom ns_geom(const ConvTcArgs& a) {
+  NsGeom g;
+  while (g.FN < a.F) g.FN *= 2;
+  g.gC = a.s2d ? 4 * a.C : a.C;
+  g.gH = a.s2d ? (a.H + 1) / 2 : a.H;
+  g.gW = a.s2d ? (a.W + 1) / 2 : a.W;
+  g.gR = a.s2d ? (a.R + 1) / 2 : a.R;
+  g.gS = a.s2d ? (a.S + 1) / 2 : a.S;
+  g.nck = (g.gC + 31) / 32;
+  g.w_bytes = static_cast<size_t>(g.gR) * g.nck * g.gS * g.FN * 128;
+  g.a_bytes = static_cast<size_t>(kNsRows + g.gR - 1) * 4096;
   // output columns per tile: at most 32 - (S - 1), balanced over the row (56 -> 2 x 28); with
   // 16 B-multiple output rows the epilogue stores through TMA, which needs valid_w % 4 == 0
-  const bool tma_store = a.OW % 4 == 0;
-  const int vmax = tma_store ? (kNsCols - (gS - 1)) & ~3 : kNsCols - (gS - 1);
-  const int tiles_w = (a.OW + vmax - 1) / vmax;
-  int valid_w = (a.OW + tiles_w - 1) / tiles_w;
-  if (tma_store) valid_w = (valid_w + 3) & ~3;
-  const int tiles_h = (a.OH + kNsRows - 1) / kNsRows;
-  const int total = a.N * tiles_h * tiles_w;
-  const size_t stage_o = kNsEpi * 8 * kNsCols * sizeof(float);  // epilogue staging (TMA-store path)
-  const size_t budget = 227 * 1024 - 2048 - stage_o;
-  int stages = static_cast<int>((budget - w_bytes) / a_bytes);
-  if (stages > 6) stages = 6;
-  const int grid = std::min(total, a.sms);
-  if (!a.maps_ready) {
-    const uint64_t dw[3] = {static_cast<uint64_t>(gC), static_cast<uint64_t>(a.F), static_cast<uint64_t>(gR) * gS};
-    const uint64_t sw[2] = {static_cast<uint64_t>(gC) * 4, static_cast<uint64_t>(gC) * a.F * 4};
-    const uint32_t bw[3] = {32, static_cast<uint32_t>(FN), 1};
-    encode_map(&a.mapW, false, true, a.ws_w, 3, dw, sw, bw);
-    // NHWC copy viewed as (c, w, h, n): box {32, 32, 4 + R - 1, 1} -> rows hh*32 + w
-    const uint64_t dx[4] = {static_cast<uint64_t>(gC), static_cast<uint64_t>(gW), static_cast<uint64_t>(gH),
-                            static_cast<uint64_t>(a.N)};
-    const uint64_t sx[3] = {static_cast<uint64_t>(gC) * 4, static_cast<uint64_t>(gW) * gC * 4,
-                            static_cast<uint64_t>(gH) * gW * gC * 4};
-    const uint32_t bx[4] = {32, kNsCols, static_cast<uint32_t>(kNsRows + gR - 1), 1};
-    encode_map(&a.mapX, false, true, a.ws_x, 4, dx, sx, bx);
-    a.maps_ready = true;
-  }
-  if (tma_store && O != a.last_O) {  // NCHW output as (w, h, f, n): box {valid_w, 1, 16, 1}
+  g.tma_store = a.OW % 4 == 0;
+  const int vmax = g.tma_store ? (kNsCols - (g.gS - 1)) & ~3 : kNsCols - (g.gS - 1);
+  g.tiles_w = (a.OW + vmax - 1) / vmax;
+  g.valid_w = (a.OW + g.tiles_w - 1) / g.tiles_w;
+  if (g.tma_store) g.valid_w = (g.valid_w + 3) & ~3;
+  g.tiles_h = (a.OH + kNsRows - 1) / kNsRows;
+  g.total = a.N * g.tiles_h * g.tiles_w;
+  g.stage_o = kNsEpi * 8 * kNsCols * sizeof(float);  // epilogue staging (TMA-store path)
+  const size_t budget = 227 * 1024 - 2048 - g.stage_o;
+  g.stages = static_cast<int>((budget - g.w_bytes) / g.a_bytes);
+  if (g.stages > 6) g.stages = 6;
+  return g;
+}
+
+void ns_maps(const ConvTcArgs& a, void* ws, void* O, ConvTcMaps& m) {
+  const NsGeom g = ns_geom(a);
+  const uint64_t dw[3] = {static_cast<uint64_t>(g.gC), static_cast<uint64_t>(a.F), static_cast<uint64_t>(g.gR) * g.gS};
+  const uint64_t sw[2] = {static_cast<uint64_t>(g.gC) * 4, static_cast<uint64_t>(g.gC) * a.F * 4};
+  const uint32_t bw[3] = {32, static_cast<uint32_t>(g.FN), 1};
+  encode_map(&m.W, false, true, static_cast<char*>(ws) + a.w_off, 3, dw, sw, bw);
+  // NHWC copy viewed as (c, w, h, n): box {32, 32, 4 + R - 1, 1} -> rows hh*32 + w
+  const uint64_t dx[4] = {static_cast<uint64_t>(g.gC), static_cast<uint64_t>(g.gW), static_cast<uint64_t>(g.gH),
+                          static_cast<uint64_t>(a.N)};
+  const uint64_t sx[3] = {static_cast<uint64_t>(g.gC) * 4, static_cast<uint64_t>(g.gW) * g.gC * 4,
+                          static_cast<uint64_t>(g.gH) * g.gW * g.gC * 4};
+  const uint32_t bx[4] = {32, kNsCols, static_cast<uint32_t>(kNsRows + g.gR - 1), 1};
+  encode_map(&m.X, false, true, static_cast<char*>(ws) + a.x_off, 4, dx, sx, bx);
+  if (g.tma_store) {  // NCHW output as (w, h, f, n): box {valid_w, 1, 8, 1}
     const uint64_t dout[4] = {static_cast<uint64_t>(a.OW), static_cast<uint64_t>(a.OH), static_cast<uint64_t>(a.F),
                               static_cast<uint64_t>(a.N)};
     const uint64_t sout[3] = {static_cast<uint64_t>(a.OW) * 4, static_cast<uint64_t>(a.OH) * a.OW * 4,
                               static_cast<uint64_t>(a.F) * a.OH * a.OW * 4};
-    const uint32_t bout[4] = {static_cast<uint32_t>(valid_w), 1, 8, 1};
-    encode_map_swizzle(&a.mapO, false, false, O, 4, dout, sout, bout, CU_TENSOR_MAP_SWIZZLE_NONE);
-    a.last_O = O;
+    const uint32_t bout[4] = {static_cast<uint32_t>(g.valid_w), 1, 8, 1};
+    encode_map_swizzle(&m.O, false, false, O, 4, dout, sout, bout, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
+}
+
+void run_conv_ns(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const float* K, float* O, void* ws,
+                 cudaStream_t st, Marks& mk) {
+  const NsGeom g = ns_geom(a);
+  const int grid = std::min(g.total, a.sms);
+  float* ws_w = reinterpret_cast<float*>(static_cast<char*>(ws) + a.w_off);
+  float* ws_x = reinterpret_cast<float*>(static_cast<char*>(ws) + a.x_off);
   auto launch = [&](auto kern) {
-    const size_t smem = w_bytes + static_cast<size_t>(stages) * a_bytes + 1024 + stage_o + 1024;
+    const size_t smem = g.w_bytes + static_cast<size_t>(g.stages) * g.a_bytes + 1024 + g.stage_o + 1024;
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "conv_ns smem attribute");
     mk.mark(st);
-    const int64_t wt = static_cast<int64_t>(a.F) * gC * gR * gS;
+    const int64_t wt = static_cast<int64_t>(a.F) * g.gC * g.gR * g.gS;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
     if (a.s2d) {
-      const int xblocks = static_cast<int>(std::min<int64_t>(1 << 20, static_cast<int64_t>(a.N) * gH));  // a row per block
+      const int xblocks = static_cast<int>(std::min<int64_t>(1 << 20, static_cast<int64_t>(a.N) * g.gH));  // a row per block
       const size_t rsm = static_cast<size_t>(a.C) * 2 * a.W * sizeof(float);
       check_cuda(cudaFuncSetAttribute(k_s2d_prepass, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)),
                  "s2d smem attribute");
-      k_s2d_prepass<<<xblocks + wblocks, 256, rsm, st>>>(I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w),
-                                                       a.N, a.C, a.H, a.W, a.F, a.R, a.S, gH, gW, gR, gS, xblocks);
+      k_s2d_prepass<<<xblocks + wblocks, 256, rsm, st>>>(I, K, ws_x, ws_w, a.N, a.C, a.H, a.W, a.F, a.R, a.S, g.gH,
+                                                       g.gW, g.gR, g.gS, xblocks);
     } else {
-      const int band = prepass_band(a.W);
+      const int band = kPrepassBand;
       const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
       check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(pre_smem)),
                  "prepass smem attribute");
       k_conv_prepass<float><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(
-          I, K, static_cast<float*>(a.ws_x), static_cast<float*>(a.ws_w), a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
+          I, K, ws_x, ws_w, a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
     }
     check_cuda(cudaGetLastError(), "conv filter conversion launch");
     count_launch();
@@ -844,27 +834,15 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const char* trace_path = std::getenv("GENSOR_CONV_TRACE");
-    static long long* trace = nullptr;
-    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
-    if (trace) check_cuda(cudaMemsetAsync(trace, 0, 1024 * 64 * sizeof(long long), st), "trace");
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapX, a.mapW, a.mapO, tma_store ? 1 : 0, O, a.N, gC, gH, gW, a.F, FN, gR, gS, a.OH, a.OW,
-                                  tiles_h, tiles_w, total, valid_w, trace),
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, m.X, m.W, m.O, g.tma_store ? 1 : 0, O, a.N, g.gC, g.gH, g.gW, a.F, g.FN,
+                                  g.gR, g.gS, a.OH, a.OW, g.tiles_h, g.tiles_w, g.total, g.valid_w),
                "conv_ns launch");
-    if (trace) {  // developer path: synchronous dump of the last launch
-      std::vector<long long> h(static_cast<size_t>(grid) * 64);
-      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
-      if (FILE* f = std::fopen(trace_path, "w")) {
-        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
-        std::fclose(f);
-      }
-    }
     mk.mark(st);
     count_launch();
   };
   auto pick = [&](auto smax) {
     constexpr int SM = decltype(smax)::value;
-    switch (stages) {
+    switch (g.stages) {
       case 2: launch(k_conv_ns<2, SM>); break;
       case 3: launch(k_conv_ns<3, SM>); break;
       case 4: launch(k_conv_ns<4, SM>); break;
@@ -875,7 +853,7 @@ void run_conv_ns(ConvTcArgs& a, const float* I, const float* K, float* O, cudaSt
   };
   // 4 filter columns need a fourth TMEM block in registers: a separate instantiation keeps the
   // 3-column epilogue (the headline) free of its register pressure
-  if (gS > 3)
+  if (g.gS > 3)
     pick(std::integral_constant<int, 4>{});
   else
     pick(std::integral_constant<int, 3>{});
@@ -890,19 +868,13 @@ size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16) {
   return static_cast<size_t>(R) * S * nck * FN * 128 + 2 * static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
 }
 
-bool conv_tc_fits_stream(int R, int FN, bool bf16) {  // two streamed stages fit shared memory
-  (void)bf16;
-  const size_t a = static_cast<size_t>((kTH + R - 1) * kTI * kTW * 128);
-  return 2 * (a + static_cast<size_t>(R) * FN * 128) <= 227 * 1024 - 1024 - 256;
-}
-
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16) {
   const int es = bf16 ? 2 : 4;
   if (!(stride == 1 && F >= 1 && F <= 256 && (C * es) % 16 == 0 && R >= 1 && R <= 8 && S >= 1 && S <= 8)) return false;
   if (conv_tc_smem_need(C, F, R, S, bf16) <= 227 * 1024 - 1024 - 256) return true;  // resident bank
   int FN = 32;
   while (FN < F) FN *= 2;
-  return conv_tc_fits_stream(R, FN, bf16) || conv_tc_fits_stream(R, 128, bf16);  // streamed (split) blocks
+  return tc_fits_stream(R, FN) || tc_fits_stream(R, 128);  // streamed (split) blocks
 }
 
 bool conv_tc_prepass_fits(int C, int W) {  // a band of NCHW rows of all channels through smem
@@ -924,36 +896,40 @@ bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16) {
   int FN = 32;
   while (FN < F) FN *= 2;
   const size_t w_bytes = static_cast<size_t>(R) * ((C + 31) / 32) * S * FN * 128;
-  return !bf16 && stride == 1 && S >= 1 && S <= 4 && R >= 1 && R <= 8 && S * FN <= 256 &&
+  return !bf16 && stride == 1 && C % 4 == 0 && S >= 1 && S <= 4 && R >= 1 && R <= 8 && S * FN <= 256 &&
          w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
 }
 
-void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk) {
+void conv_tc_maps(const ConvTcArgs& a, void* ws, void* O, ConvTcMaps& m) {
+  if (a.ns)
+    ns_maps(a, ws, O, m);
+  else
+    tc_maps(a, ws, m);
+}
+
+void launch_conv_tc(const ConvTcArgs& a, const ConvTcMaps& m, const void* I, const void* K, void* O, void* ws,
+                    cudaStream_t st, Marks& mk) {
   const float* i = static_cast<const float*>(I);
   const float* k = static_cast<const float*>(K);
   float* o = static_cast<float*>(O);
   if (a.ns) {
-    run_conv_ns(a, i, k, o, st, mk);
+    run_conv_ns(a, m, i, k, o, ws, st, mk);
     return;
   }
-  int FN = 32;
-  while (FN < a.F) FN *= 2;
-  if (FN > 128 && !conv_tc_fits_stream(a.R, FN, a.bf16) &&
-      conv_tc_smem_need(a.C, a.F, a.R, a.S, a.bf16) > 227 * 1024 - 1024 - 256)
-    FN = 128;  // groups of 128 filters, each a tile of its own
+  const int FN = tc_geom(a).FN;
   if (a.bf16) {
     switch (FN) {
-      case 32: run_conv<__nv_bfloat16, 32>(a, i, k, o, st, mk); break;
-      case 64: run_conv<__nv_bfloat16, 64>(a, i, k, o, st, mk); break;
-      case 128: run_conv<__nv_bfloat16, 128>(a, i, k, o, st, mk); break;
-      default: run_conv<__nv_bfloat16, 256>(a, i, k, o, st, mk); break;
+      case 32: run_conv<__nv_bfloat16, 32>(a, m, i, k, o, ws, st, mk); break;
+      case 64: run_conv<__nv_bfloat16, 64>(a, m, i, k, o, ws, st, mk); break;
+      case 128: run_conv<__nv_bfloat16, 128>(a, m, i, k, o, ws, st, mk); break;
+      default: run_conv<__nv_bfloat16, 256>(a, m, i, k, o, ws, st, mk); break;
     }
   } else {
     switch (FN) {
-      case 32: run_conv<float, 32>(a, i, k, o, st, mk); break;
-      case 64: run_conv<float, 64>(a, i, k, o, st, mk); break;
-      case 128: run_conv<float, 128>(a, i, k, o, st, mk); break;
-      default: run_conv<float, 256>(a, i, k, o, st, mk); break;
+      case 32: run_conv<float, 32>(a, m, i, k, o, ws, st, mk); break;
+      case 64: run_conv<float, 64>(a, m, i, k, o, ws, st, mk); break;
+      case 128: run_conv<float, 128>(a, m, i, k, o, ws, st, mk); break;
+      default: run_conv<float, 256>(a, m, i, k, o, ws, st, mk); break;
     }
   }
 }

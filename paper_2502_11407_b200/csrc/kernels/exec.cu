@@ -7,6 +7,7 @@
 #include <sstream>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -32,8 +33,44 @@ void check_cuda(cudaError_t e, const char* what) {
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+namespace {
+// Developer A/B switches (GENSOR_* environment variables) exist only in builds compiled with
+// -DGENSOR_DEV_OVERRIDES (make DEV=1); the product library never reads the environment.
+const char* dev_env(const char* name) {
+#ifdef GENSOR_DEV_OVERRIDES
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+}  // namespace
+
 enum class Family { Generic, GemmTc, ConvTc, ConvGemm, Stream };
 
+// Tensor maps of one (inputs, output, workspace) pointer tuple. Encoding is pure host work, but
+// at a few microseconds per execute it would show on the microsecond-scale ops, so the handle
+// keeps the last few tuples (results never depend on the cache).
+struct CallMaps {
+  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool valid = false;
+  uint64_t used = 0;
+  GemmTcMaps g;
+  ConvTcMaps c;
+  CUtensorMap w;
+};
+constexpr int kMapCache = 4;
+
+// Per-stream device workspace (pre-pass outputs of the conv families): two executes of one
+// handle on different streams never share one.
+struct WsSlot {
+  cudaStream_t stream = nullptr;
+  void* ptr = nullptr;
+};
+
+// An instantiated kernel. The plan fields are immutable after prepare(); execute() only touches
+// the mutex-guarded caches (workspace slots, tensor maps), so one handle may be executed from
+// several threads / streams at once (include/gensor_b200.h).
 struct Kernel {
   OpDesc op;
   Sched state;
@@ -47,12 +84,18 @@ struct Kernel {
   StreamArgs stream;
   int launches = 1;
   std::vector<std::string> launch_names{"generic_simt"};
-  bool timing = false;
-  cudaEvent_t ev[8] = {};
-  int marks_used = 0;
   std::string plan_info;
-  void* ws = nullptr;  // family workspace
-  // host-buffer execute staging (allocated on first use)
+  size_t ws_bytes = 0;  // device workspace one execute needs (0: none)
+  mutable std::mutex mu;
+  mutable std::vector<WsSlot> ws_slots;
+  mutable CallMaps maps[kMapCache];
+  mutable uint64_t map_clock = 0;
+  // per-launch timing instrumentation (gensor_kernel_set_timing): events recorded around each
+  // internal launch of the executes issued while it is on; meant for one stream at a time
+  mutable bool timing = false;
+  mutable cudaEvent_t ev[8] = {};
+  mutable int marks_used = 0;
+  // host-buffer execute staging (gensor_execute_host takes a non-const handle: one call at a time)
   void* d_in[3] = {nullptr, nullptr, nullptr};
   void* d_out = nullptr;
   struct HostPipe* pipe = nullptr;  // chunked copy/compute overlap for execute_host (lazy)
@@ -219,7 +262,7 @@ bool gemm_tc_ok(const OpDesc& op, bool bf16) {
 // conv_ns (tf32, stride 1, S <= 3, S*F <= 256): NCHW in place, filter columns folded into N
 bool conv_ns_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16) return false;
-  if (std::getenv("GENSOR_CONV_NS") && std::string(std::getenv("GENSOR_CONV_NS")) == "0") return false;  // A/B
+  if (dev_env("GENSOR_CONV_NS") && dev_env("GENSOR_CONV_NS")[0] == '0') return false;  // A/B
   return conv_ns_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
                            static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
                            static_cast<int>(op.stride), bf16) &&
@@ -229,7 +272,7 @@ bool conv_ns_ok(const OpDesc& op, bool bf16) {
 // stride-2 convs with few channels (ResNet stem): conv_ns over the space-to-depth form
 bool conv_s2d_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16) return false;
-  if (std::getenv("GENSOR_CONV_S2D") && std::getenv("GENSOR_CONV_S2D")[0] == '0') return false;  // A/B
+  if (dev_env("GENSOR_CONV_S2D") && dev_env("GENSOR_CONV_S2D")[0] == '0') return false;  // A/B
   return conv_s2d_supported(static_cast<int>(op.param("C")), static_cast<int>(op.param("F")),
                             static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
                             static_cast<int>(op.stride), bf16);
@@ -253,7 +296,7 @@ bool conv_tc_ok(const OpDesc& op, bool bf16) {
 bool conv1x1_gemm_ok(const OpDesc& op, bool bf16) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16 || op.stride != 1) return false;
   if (op.param("R") != 1 || op.param("S") != 1) return false;
-  if (std::getenv("GENSOR_CONV1X1_GEMM") && std::getenv("GENSOR_CONV1X1_GEMM")[0] == '0') return false;  // A/B
+  if (dev_env("GENSOR_CONV1X1_GEMM") && dev_env("GENSOR_CONV1X1_GEMM")[0] == '0') return false;  // A/B
   const int64_t P = op.param("H") * op.param("W");
   // per-image N tiles of 128 positions: small planes (14x14 -> 77 % of the tile used) stay with
   // conv_gemm, which flattens the positions of all images into M (measured on ResNet-50)
@@ -306,6 +349,10 @@ DeviceLimits query(int device) {
 
 Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
   if (!s.complete()) throw Error(Code::IncompleteState, "kernel needs a complete schedule");
+  // the kernels read fp32 (dtype_bytes 4) or bf16 (dtype_bytes 2) storage only
+  if (op.dtype_bytes != 2 && op.dtype_bytes != 4)
+    throw Error(Code::Unsupported, "dtype_bytes " + std::to_string(op.dtype_bytes) +
+                                       " has no kernel: execute supports 4 (fp32) and 2 (bf16)");
   auto* k = new Kernel;
   k->op = op;
   k->state = s;
@@ -352,41 +399,23 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           int bn = static_cast<int>(pow2_clamp(s.L && !conv1x1 ? s.tile(op, 1, 1) : 128, 64, bn_max));
           auto tiles = [&](int b) { return static_cast<int64_t>((g.M + 127) / 128) * ((g.N + b - 1) / b) * g.batch; };
           while (bn > 64 && tiles(bn) < sms) bn /= 2;
-          if (const char* e = std::getenv("GENSOR_GEMM_BN")) bn = std::atoi(e);  // developer override
+          if (const char* e = dev_env("GENSOR_GEMM_BN")) bn = std::atoi(e);
           g.BN = bn;
           g.sms = sms;
-          // A multicast across clusters of n-tiles (GENSOR_GEMM_CLUSTER=2|4): measured not to pay on
-          // the suite shapes (G: 16.2 vs 15.0 us, GPT-2 sequence -7 %) — the k-loop is not L2 bound
-          static const int cs_env = std::getenv("GENSOR_GEMM_CLUSTER") ? std::atoi(std::getenv("GENSOR_GEMM_CLUSTER")) : 1;
+          const int nkb = (g.K * op.dtype_bytes + 127) / 128;
+          g.stages = std::min(gemm_tc_max_stages(bn, bf16), nkb > 8 ? 8 : nkb > 4 ? 6 : 4);
+          // A multicast across clusters of n-tiles (developer switch GENSOR_GEMM_CLUSTER=2|4):
+          // measured not to pay on the suite shapes (G: 16.2 vs 15.0 us, GPT-2 sequence -7 %)
+          const int cs_env = dev_env("GENSOR_GEMM_CLUSTER") ? std::atoi(dev_env("GENSOR_GEMM_CLUSTER")) : 1;
           const int tn = (g.N + bn - 1) / bn;
           g.cs = (cs_env >= 4 && tn % 4 == 0) ? 4 : (cs_env >= 2 && tn % 2 == 0) ? 2 : 1;
-          // split-K (GENSOR_GEMM_SPLITK=1) for fp32 output when the tile grid leaves half the SMs
-          // idle: BN 128 tiles x k-splits, partials added by the tile's owner in a fixed order.
-          // Measured slower on G (22.5 vs 15.3 us: the owner's partial reads are latency bound),
-          // so off by default.
-          static const bool splitk_env = std::getenv("GENSOR_GEMM_SPLITK") != nullptr;
-          const int nkb = (g.K * op.dtype_bytes + 127) / 128;
-          if (splitk_env && !bf16 && g.cs == 1 && nkb >= 16) {
-            const int64_t t128 = static_cast<int64_t>((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
-            int sp = 1;
-            while (sp < 4 && t128 * sp * 2 <= sms && nkb / (sp * 2) >= 8) sp *= 2;
-            if (sp > 1) {
-              g.BN = 128;
-              g.splits = sp;
-              const size_t pb = static_cast<size_t>(t128) * (sp - 1) * 128 * 128 * 4;
-              check_cuda(cudaMalloc(&k->ws, pb + static_cast<size_t>(t128) * 8), "gemm split-K workspace");
-              g.partials = static_cast<float*>(k->ws);
-              g.flags = reinterpret_cast<unsigned long long*>(static_cast<char*>(k->ws) + pb);
-              check_cuda(cudaMemset(g.flags, 0, static_cast<size_t>(t128) * 8), "gemm split-K flags");
-            }
-          }
           pi << "{\"family\":\"gemm_tc\"" << (conv1x1 ? ",\"conv1x1\":\"O[n] = K . I[n], filter bank shared\"" : "")
-             << ",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"tiles\":" << tiles(g.BN)
-             << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms) << ",\"block\":192,\"persistent\":true"
-             << ",\"cluster_n\":" << g.cs << ",\"split_k\":" << g.splits << "}";
+             << ",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"stages\":" << gemm_tc_stages(g)
+             << ",\"tiles\":" << tiles(g.BN) << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms)
+             << ",\"block\":192,\"persistent\":true,\"cluster_n\":" << g.cs << "}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16) &&
-                   !(std::getenv("GENSOR_CONV_FAMILY") && std::string(std::getenv("GENSOR_CONV_FAMILY")) == "gemm" &&
-                     !bf16)) {  // developer override: A/B the two conv families on one shape
+                   !(dev_env("GENSOR_CONV_FAMILY") && std::string(dev_env("GENSOR_CONV_FAMILY")) == "gemm" &&
+                     !bf16)) {  // developer switch: A/B the two conv families on one shape
           k->family = Family::ConvTc;
           k->launches = 1;
           k->launch_names = {"conv_tc"};
@@ -411,9 +440,10 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
             xb = static_cast<size_t>(c.N) * ((c.H + 1) / 2) * ((c.W + 1) / 2) * 4 * c.C * es;
             wb = static_cast<size_t>((c.R + 1) / 2) * ((c.S + 1) / 2) * c.F * 4 * c.C * es;
           }
-          check_cuda(cudaMalloc(&k->ws, ((wb + 255) & ~size_t(255)) + xb), "conv workspace");
-          c.ws_w = k->ws;
-          c.ws_x = static_cast<char*>(k->ws) + ((wb + 255) & ~size_t(255));
+          c.w_off = 0;
+          c.x_off = (wb + 255) & ~size_t(255);
+          c.ws_bytes = c.x_off + xb;
+          k->ws_bytes = c.ws_bytes;
           k->launches = 2;  // filter conversion + conv (programmatic dependent launch), timed as one span
           k->launch_names = {c.ns ? "conv_ns" : "conv_tc"};
           if (c.ns) {
@@ -457,8 +487,8 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           c.packed = c.C * c.S <= 64 && c.C < 32;
           const int Cp = c.packed ? (c.S * c.C + 3) / 4 * 4 : (c.C + 3) / 4 * 4;
           const size_t planes = c.packed ? c.R : static_cast<size_t>(c.R) * c.S;
-          check_cuda(cudaMalloc(&k->ws, planes * c.F * Cp * 4), "conv_gemm workspace");
-          c.ws_w = k->ws;
+          c.ws_bytes = planes * c.F * Cp * 4;
+          k->ws_bytes = c.ws_bytes;
           const int64_t P = static_cast<int64_t>(c.N) * c.OH * c.OW;
           const int64_t tiles = ((P + 127) / 128) * ((c.F + bn - 1) / bn);
           pi << "{\"family\":\"conv_gemm\",\"BM\":128,\"BN\":" << bn << ",\"tiles\":" << tiles
@@ -493,7 +523,6 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         throw Error(Code::Unsupported, "variant " + std::to_string(variant) + " not available for " + op.label());
     }
   } catch (...) {
-    if (k->ws) cudaFree(k->ws);
     delete k;
     throw;
   }
@@ -516,7 +545,8 @@ void destroy(Kernel* k) {
   for (void* p : k->d_in)
     if (p) cudaFree(p);
   if (k->d_out) cudaFree(k->d_out);
-  if (k->ws) cudaFree(k->ws);
+  for (const WsSlot& w : k->ws_slots)
+    if (w.ptr) cudaFree(w.ptr);
   for (auto& e : k->ev)
     if (e) cudaEventDestroy(e);
   delete k;
@@ -535,8 +565,67 @@ std::string info(const Kernel* k) {
   return os.str();
 }
 
-void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, void* stream) {
-  auto* k = const_cast<Kernel*>(kc);  // tensor-map caches only; results do not depend on them
+size_t workspace_bytes(const Kernel* k) { return k->ws_bytes; }
+
+namespace {
+
+// The calling stream's workspace slot, allocated on the stream's first execute. A first execute
+// inside a stream capture allocates in relaxed capture mode (the allocation is not captured).
+void* stream_workspace(const Kernel* k, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(k->mu);
+  for (const WsSlot& w : k->ws_slots)
+    if (w.stream == st) return w.ptr;
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  check_cuda(cudaThreadExchangeStreamCaptureMode(&mode), "capture mode");
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, k->ws_bytes);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  check_cuda(e, "kernel workspace");
+  k->ws_slots.push_back({st, p});
+  return p;
+}
+
+// Tensor maps of this call's pointers (cached per pointer tuple).
+void call_maps(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* ws, CallMaps& out) {
+  const void* key[4] = {d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out, ws};
+  std::lock_guard<std::mutex> lock(k->mu);
+  CallMaps* slot = &k->maps[0];
+  for (CallMaps& m : k->maps) {
+    if (m.valid && std::memcmp(m.key, key, sizeof key) == 0) {
+      m.used = ++k->map_clock;
+      out = m;
+      return;
+    }
+    if (!m.valid || m.used < slot->used) slot = &m;
+  }
+  CallMaps fresh;
+  std::memcpy(fresh.key, key, sizeof key);
+  switch (k->family) {
+    case Family::GemmTc:  // 1x1 conv: inputs are (I, K) but the GEMM is K . I
+      if (k->gemm.a_shared)
+        gemm_tc_maps(k->gemm, d_in[1], d_in[0], d_out, fresh.g);
+      else
+        gemm_tc_maps(k->gemm, d_in[0], d_in[1], d_out, fresh.g);
+      break;
+    case Family::ConvTc:
+      conv_tc_maps(k->conv, ws, d_out, fresh.c);
+      break;
+    case Family::ConvGemm:
+      conv_gemm_map(k->cgemm, ws, fresh.w);
+      break;
+    default:
+      break;
+  }
+  fresh.valid = true;
+  fresh.used = ++k->map_clock;
+  *slot = fresh;
+  out = fresh;
+}
+
+}  // namespace
+
+void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* ws, size_t ws_size,
+             void* stream) {
   const OpDesc& op = k->op;
   if (n_in != op.input_count())
     throw Error(Code::ShapeMismatch,
@@ -544,6 +633,13 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
   for (int i = 0; i < n_in; ++i)
     if (!d_in[i]) throw Error(Code::ShapeMismatch, "null input pointer");
   auto st = static_cast<cudaStream_t>(stream);
+  if (k->ws_bytes) {
+    if (!ws)
+      ws = stream_workspace(k, st);
+    else if (ws_size < k->ws_bytes)
+      throw Error(Code::ShapeMismatch, "workspace of " + std::to_string(ws_size) + " bytes, the kernel needs " +
+                                     std::to_string(k->ws_bytes));
+  }
   Marks mk;
   if (k->timing) mk.ev = k->ev;
   switch (k->family) {
@@ -553,42 +649,47 @@ void execute(const Kernel* kc, const void* const* d_in, int n_in, void* d_out, v
                      static_cast<int>(op.batch), st);
       mk.mark(st);
       break;
-    case Family::GemmTc:
+    case Family::GemmTc: {
+      CallMaps m;
+      call_maps(k, d_in, n_in, d_out, ws, m);
       mk.mark(st);
-      // 1x1 conv: inputs are (I, K) but the GEMM is K . I
-      if (k->gemm.a_shared)
-        launch_gemm_tc(k->gemm, d_in[1], d_in[0], d_out, st);
-      else
-        launch_gemm_tc(k->gemm, d_in[0], d_in[1], d_out, st);
+      launch_gemm_tc(k->gemm, m.g, st);
       mk.mark(st);
       break;
-    case Family::ConvTc:
-      launch_conv_tc(k->conv, d_in[0], d_in[1], d_out, st, mk);
+    }
+    case Family::ConvTc: {
+      CallMaps m;
+      call_maps(k, d_in, n_in, d_out, ws, m);
+      launch_conv_tc(k->conv, m.c, d_in[0], d_in[1], d_out, ws, st, mk);
       break;
-    case Family::ConvGemm:
-      launch_conv_gemm(k->cgemm, d_in[0], d_in[1], d_out, st, mk);
+    }
+    case Family::ConvGemm: {
+      CallMaps m;
+      call_maps(k, d_in, n_in, d_out, ws, m);
+      launch_conv_gemm(k->cgemm, m.w, d_in[0], d_in[1], d_out, ws, st, mk);
       break;
+    }
     case Family::Stream:
       mk.mark(st);
       launch_stream(k->stream, d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out, st);
       mk.mark(st);
       break;
   }
-  k->marks_used = mk.next;
+  if (k->timing) k->marks_used = mk.next;
 }
 
 // Median device time (ms) of `iters` executes, CUDA events on `stream` around each one (after one
 // untimed warm-up execute). Used by the on-device re-ranking of the top-k schedules.
 float time_execute(Kernel* k, const void* const* d_in, int n_in, void* d_out, void* stream, int iters) {
   auto st = static_cast<cudaStream_t>(stream);
-  execute(k, d_in, n_in, d_out, stream);
+  execute(k, d_in, n_in, d_out, nullptr, 0, stream);
   cudaEvent_t a, b;
   check_cuda(cudaEventCreate(&a), "cudaEventCreate");
   check_cuda(cudaEventCreate(&b), "cudaEventCreate");
   std::vector<float> ms;
   for (int i = 0; i < std::max(1, iters); ++i) {
     check_cuda(cudaEventRecord(a, st), "cudaEventRecord");
-    execute(k, d_in, n_in, d_out, stream);
+    execute(k, d_in, n_in, d_out, nullptr, 0, stream);
     check_cuda(cudaEventRecord(b, st), "cudaEventRecord");
     check_cuda(cudaEventSynchronize(b), "cudaEventSynchronize");
     float t = 0.f;
@@ -673,7 +774,7 @@ void plan_pipe(Kernel* k) {
   const int nin = op.input_count();
   size_t total = 0;
   for (int t = 0; t <= nin; ++t) total += tensor_bytes(op, t);
-  static const bool off = std::getenv("GENSOR_HOST_PIPE") && std::getenv("GENSOR_HOST_PIPE")[0] == '0';
+  const bool off = dev_env("GENSOR_HOST_PIPE") && dev_env("GENSOR_HOST_PIPE")[0] == '0';
   if (off || total < (size_t(8) << 20)) return;  // small ops: one copy, one launch, one copy
   switch (op.kind) {
     case Kind::Gemm:
@@ -695,7 +796,7 @@ void plan_pipe(Kernel* k) {
   }
   if (hp->extent < 2) return;
   // chunks of ~9 MB of traffic (measured: PCIe reaches full duplex only for multi-MB copies), <= 16
-  static const int chunk_mb = std::getenv("GENSOR_HOST_PIPE_MB") ? std::atoi(std::getenv("GENSOR_HOST_PIPE_MB")) : 9;
+  const int chunk_mb = dev_env("GENSOR_HOST_PIPE_MB") ? std::atoi(dev_env("GENSOR_HOST_PIPE_MB")) : 9;
   int64_t chunks = std::min<int64_t>({hp->extent, 16, static_cast<int64_t>(total / (size_t(std::max(1, chunk_mb)) << 20))});
   if (chunks < 2) return;
   hp->q = (hp->extent + chunks - 1) / chunks;
@@ -736,7 +837,7 @@ void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, voi
     try {
       plan_pipe(k);
     } catch (const Error& e) {  // a chunk shape the family cannot run: keep the one-shot path
-      if (std::getenv("GENSOR_HOST_PIPE_DEBUG")) std::fprintf(stderr, "host pipe disabled: %s\n", e.what());
+      if (dev_env("GENSOR_HOST_PIPE_DEBUG")) std::fprintf(stderr, "host pipe disabled: %s\n", e.what());
       if (k->pipe) {
         for (Kernel*& sk : k->pipe->sub) {
           destroy(sk);
@@ -751,7 +852,7 @@ void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, voi
     for (int i = 0; i < n_in; ++i)
       if (!k->d_in[i]) check_cuda(cudaMalloc(&k->d_in[i], tensor_bytes(op, i)), "cudaMalloc input staging");
     if (!k->d_out) check_cuda(cudaMalloc(&k->d_out, tensor_bytes(op, op.output_index())), "cudaMalloc output staging");
-    static const bool dbg = std::getenv("GENSOR_HOST_PIPE_DEBUG") != nullptr;
+    const bool dbg = dev_env("GENSOR_HOST_PIPE_DEBUG") != nullptr;
     std::vector<cudaEvent_t> dev_t(dbg ? 3 * hp.ev_in.size() : 0);
     cudaEvent_t dev_t0 = nullptr;
     if (dbg) {
@@ -788,7 +889,7 @@ void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, voi
       if (dbg) cudaEventRecord(dev_t[3 * c], hp.s_in);
       check_cuda(cudaStreamWaitEvent(st, hp.ev_in[static_cast<size_t>(c)], 0), "pipe wait");
       const size_t ooff = static_cast<size_t>(u0) * hp.unit_bytes[3], ob = static_cast<size_t>(cnt) * hp.unit_bytes[3];
-      execute(sk, din, n_in, static_cast<char*>(k->d_out) + ooff, st);
+      execute(sk, din, n_in, static_cast<char*>(k->d_out) + ooff, nullptr, 0, st);
       check_cuda(cudaEventRecord(hp.ev_k[static_cast<size_t>(c)], st), "pipe event");
       if (dbg) cudaEventRecord(dev_t[3 * c + 1], st);
       check_cuda(cudaStreamWaitEvent(hp.s_out, hp.ev_k[static_cast<size_t>(c)], 0), "pipe wait");
@@ -818,7 +919,7 @@ void execute_host(Kernel* k, const void* const* h_in, int n_in, void* h_out, voi
   }
   const size_t ob = tensor_bytes(op, op.output_index());
   if (!k->d_out) check_cuda(cudaMalloc(&k->d_out, ob), "cudaMalloc output staging");
-  execute(k, k->d_in, n_in, k->d_out, stream);
+  execute(k, k->d_in, n_in, k->d_out, nullptr, 0, stream);
   check_cuda(cudaMemcpyAsync(h_out, k->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
   check_cuda(cudaStreamSynchronize(st), "stream sync");
 }

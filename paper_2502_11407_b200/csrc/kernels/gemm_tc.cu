@@ -8,9 +8,7 @@
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns -> registers -> global (fp32 or bf16).
 #include <cuda_bf16.h>
 
-#include <cstdio>
-#include <cstdlib>
-#include <vector>
+#include <algorithm>
 #include <cudaTypedefs.h>
 
 #include "../host/error.hpp"
@@ -49,10 +47,7 @@ template <typename T, typename TOut, int BN, int STAGES, int CS, int SB>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
-              long long* __restrict__ trace, int splits, float* __restrict__ partials,
-              unsigned long long* __restrict__ flags, unsigned long long flag_target, int a_batched) {
-#define GEMM_TRACE(slot, v) \
-  if (trace) trace[blockIdx.x * 64 + (slot)] = (v)
+              int a_batched) {
   constexpr int BM = 128;
   constexpr int BK = 128 / sizeof(T);           // K elements per 128 B swizzle row
   constexpr uint32_t A_BYTES = BM * 128;
@@ -82,13 +77,8 @@ __global__ void __launch_bounds__(192, 1)
   // tile (group's m, group's n * CS + r). CS = 1 is the plain persistent walk.
   const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int cid = blockIdx.x / CS, nclusters = gridDim.x / CS;
-  // split-K (splits > 1, CS == 1): work unit = (tile, k-split); the units of splits S-1..1 come
-  // first and the owners (split 0, which add the partials and store C) last, so an owner only
-  // ever waits on units that are running or done — never on one queued behind it
-  const int groups = total / CS * splits;
-  auto tile_of = [&](int gi) { return (gi % (total / CS)) * CS + rank; };
-  auto split_of = [&](int gi) { return splits - 1 - gi / (total / CS); };
-  auto kb_lo = [&](int sp) { return static_cast<int>(static_cast<int64_t>(nk) * sp / splits); };
+  const int groups = total / CS;
+  auto tile_of = [&](int gi) { return gi * CS + rank; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -116,19 +106,14 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (elect_one()) {
       int it = 0;
-      long long pw = 0;
-      GEMM_TRACE(10, clock64());
       for (int gi = cid; gi < groups; gi += nclusters) {
-        const int t = tile_of(gi), sp = split_of(gi);
+        const int t = tile_of(gi);
         const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
         const int m0 = mt * BM, n0 = nt * BN;
-        for (int kb = kb_lo(sp); kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          const long long w0 = trace ? clock64() : 0;
           mbar_wait(&empty[s], ph ^ 1);
-          if (trace) pw += clock64() - w0;
-          if (it < 40) GEMM_TRACE(20 + it, clock64());
           mbar_arrive_expect_tx(&full[s], STAGE);
           uint8_t* a_s = smem + s * STAGE;
           uint8_t* b_s = a_s + A_BYTES;
@@ -137,30 +122,23 @@ __global__ void __launch_bounds__(192, 1)
                            static_cast<uint16_t>((1u << CS) - 1));
           else
             tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b * a_batched);  // 0: A shared by the batch
-          (void)0;
 #pragma unroll
           for (int j = 0; j < B_CHUNKS; ++j)
             tma_load_3d(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
         }
       }
-      GEMM_TRACE(61, pw);
     }
   } else if (warp == 1) {
     if (elect_one()) {
       int it = 0, local = 0;
-      long long fw = 0;
-      GEMM_TRACE(0, clock64());
       for (int gi = cid; gi < groups; gi += nclusters, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        const int sp = split_of(gi), kb0 = kb_lo(sp);
-        for (int kb = kb0; kb < kb_lo(sp + 1); ++kb, ++it) {
+        for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
-          const long long w0 = trace ? clock64() : 0;
           mbar_wait(&full[s], (it / STAGES) & 1);
-          if (trace) fw += clock64() - w0;
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * STAGE);
           const uint32_t b_addr = a_addr + A_BYTES;
@@ -172,9 +150,9 @@ __global__ void __launch_bounds__(192, 1)
                                     ? smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 1024, 2)
                                     : smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 512, 1);
             if constexpr (TcTraits<T>::kF16Kind)
-              mma_f16(d, ad, bd, IDESC, ((kb - kb0) | k) != 0);
+              mma_f16(d, ad, bd, IDESC, (kb | k) != 0);
             else
-              mma_tf32(d, ad, bd, IDESC, ((kb - kb0) | k) != 0);
+              mma_tf32(d, ad, bd, IDESC, (kb | k) != 0);
           }
           if constexpr (CS > 1)
             mma_commit_mc(&empty[s], static_cast<uint16_t>((1u << CS) - 1));
@@ -182,9 +160,7 @@ __global__ void __launch_bounds__(192, 1)
             mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[acc]);
-        if (local < 4) GEMM_TRACE(1 + local, clock64());
       }
-      GEMM_TRACE(60, fw);
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter this warp may access = its 32 tile rows
@@ -192,46 +168,12 @@ __global__ void __launch_bounds__(192, 1)
     // stores still read (short k-loops: the epilogue is the critical path)
     int local = 0;
     for (int gi = cid; gi < groups; gi += nclusters, ++local) {
-      const int t = tile_of(gi), sp = split_of(gi);
+      const int t = tile_of(gi);
       const int acc = local & 1;
       const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
       const int m0 = mt * BM, n0 = nt * BN;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
-      if (sp > 0) {  // split-K partner: this warp's 32 rows of the partial tile -> workspace
-        if constexpr (sizeof(TOut) == 4) {
-          float* prow = partials + ((static_cast<int64_t>(t) * (splits - 1) + sp - 1) * BM + q * 32 + lane) * BN;
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<uint4*>(prow + c + 4 * k) = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
-          }
-          tc_fence_before();
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&acc_empty[acc]);
-            atomicAdd(&flags[t], 1ULL);  // 4 warps x (splits - 1) partners publish per tile
-          }
-        }
-        continue;
-      }
-      float part_scale = splits > 1 ? 1.0f : 0.0f;  // owner: add the partner splits' partials
-      if (splits > 1) {
-        if (lane == 0)
-          while (true) {
-            unsigned long long v;
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + t) : "memory");
-            if (v >= flag_target) break;
-            __nanosleep(64);
-          }
-        __syncwarp();
-        __threadfence();
-      }
       uint8_t* stg = staging + (q * SB + (local % SB)) * STG_WARP;
       if (lane == 0) bulk_wait_read<SB - 1>();  // the stores that last read this slice are done
       __syncwarp();
@@ -240,20 +182,6 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[32];
         tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
-        if (part_scale != 0.0f) {  // fixed order: split 1, 2, ... (deterministic)
-          for (int sp2 = 1; sp2 < splits; ++sp2) {
-            const float* prow =
-                partials + ((static_cast<int64_t>(t) * (splits - 1) + sp2 - 1) * BM + q * 32 + lane) * BN + c;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float4 pv = __ldcg(reinterpret_cast<const float4*>(prow) + k);
-              r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + pv.x);
-              r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + pv.y);
-              r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + pv.z);
-              r[4 * k + 3] = __float_as_uint(__uint_as_float(r[4 * k + 3]) + pv.w);
-            }
-          }
-        }
         if constexpr (sizeof(TOut) == 4) {  // 32 fp32 = one 128 B block, 8 chunks
           uint8_t* blk = stg + (c / 32) * (32 * 128) + lane * 128;
 #pragma unroll
@@ -288,10 +216,8 @@ __global__ void __launch_bounds__(192, 1)
         }
         bulk_commit();
       }
-      if (warp == 2 && lane == 0 && local < 4) GEMM_TRACE(6 + local, clock64());
     }
     if (lane == 0) bulk_wait<0>();
-    if (warp == 2 && lane == 0) GEMM_TRACE(9, clock64());
   }
   tc_fence_before();
   __syncthreads();
@@ -315,7 +241,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <typename T, typename TOut, int BN, int STAGES, int CS, int SB = 1>
-void run_cs(GemmTcArgs& a, cudaStream_t st) {
+void run_cs(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
   const size_t smem = STAGES * STAGE + SB * 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
   auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS, SB>;
@@ -325,23 +251,8 @@ void run_cs(GemmTcArgs& a, cudaStream_t st) {
   const int total = tiles_m * tiles_n * a.batch;
   if constexpr (CS == 1) {
     const int grid = std::min(total, a.sms);
-    static const char* trace_path = std::getenv("GENSOR_GEMM_TRACE");
-    static long long* trace = nullptr;
-    if (trace_path && !trace) check_cuda(cudaMalloc(&trace, 1024 * 64 * sizeof(long long)), "trace");
-    const int units = total * a.splits;
-    const int grid_u = std::min(units, a.sms);
-    if (a.splits > 1) a.flag_target += 4ULL * (a.splits - 1);
-    kern<<<grid_u, 192, smem, st>>>(a.mapA, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total, trace, a.splits,
-                                    a.partials, a.flags, a.flag_target, a.a_shared ? 0 : 1);
+    kern<<<grid, 192, smem, st>>>(m.A, m.B, m.C, a.M, a.N, a.K, tiles_m, tiles_n, total, a.a_shared ? 0 : 1);
     check_cuda(cudaGetLastError(), "gemm_tc launch");
-    if (trace) {  // developer path: synchronous dump of the last launch
-      std::vector<long long> h(static_cast<size_t>(grid) * 64);
-      check_cuda(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "trace");
-      if (FILE* f = std::fopen(trace_path, "w")) {
-        for (size_t i = 0; i < h.size(); ++i) std::fprintf(f, "%lld%c", h[i], (i % 64) == 63 ? '\n' : ' ');
-        std::fclose(f);
-      }
-    }
   } else {
     const int grid = std::min(total, a.sms / CS * CS);
     cudaLaunchConfig_t cfg = {};
@@ -356,9 +267,8 @@ void run_cs(GemmTcArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    check_cuda(cudaLaunchKernelEx(&cfg, kern, a.mapAm, a.mapB, a.mapC, a.M, a.N, a.K, tiles_m, tiles_n, total,
-                                  static_cast<long long*>(nullptr), 1, static_cast<float*>(nullptr),
-                                  static_cast<unsigned long long*>(nullptr), 0ULL, a.a_shared ? 0 : 1),
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, m.Am, m.B, m.C, a.M, a.N, a.K, tiles_m, tiles_n, total,
+                                  a.a_shared ? 0 : 1),
                "gemm_tc cluster launch");
   }
   count_launch();
@@ -367,43 +277,44 @@ void run_cs(GemmTcArgs& a, cudaStream_t st) {
 // Cluster multicast of A pays when the k-loop is long (A re-read from L2 for every n-tile) and
 // the n-tiles split into whole clusters; CS = cluster size along N.
 template <typename T, typename TOut, int BN, int STAGES>
-void run(GemmTcArgs& a, cudaStream_t st) {
+void run(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   const int tiles_n = (a.N + BN - 1) / BN;
   constexpr size_t STAGE = 128 * 128 + BN * 128;
   constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
   const int nk = (a.K + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T));
   if constexpr (2 * STAGE + 2 * STG + 2048 <= 227 * 1024) {
     if (nk <= 2 && a.cs == 1) {  // epilogue-bound: double-buffered staging, 2 pipeline stages
-      run_cs<T, TOut, BN, 2, 1, 2>(a, st);
+      run_cs<T, TOut, BN, 2, 1, 2>(a, m, st);
       return;
     }
   }
   if (a.cs == 4 && tiles_n % 4 == 0)
-    run_cs<T, TOut, BN, STAGES, 4>(a, st);
+    run_cs<T, TOut, BN, STAGES, 4>(a, m, st);
   else if (a.cs >= 2 && tiles_n % 2 == 0)
-    run_cs<T, TOut, BN, STAGES, 2>(a, st);
+    run_cs<T, TOut, BN, STAGES, 2>(a, m, st);
   else
-    run_cs<T, TOut, BN, STAGES, 1>(a, st);
+    run_cs<T, TOut, BN, STAGES, 1>(a, m, st);
 }
 
-// Pipeline depth: as many stages as fit next to the epilogue staging (227 KB opt-in).
+// Pipeline depth: the plan's stage count (from the schedule), capped by what fits next to the
+// epilogue staging (227 KB opt-in) and by the k-loop length.
 template <typename T, typename TOut, int BN>
-void run_bn(GemmTcArgs& a, cudaStream_t st) {
+void run_bn(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   constexpr size_t STAGE = 128 * 128 + BN * 128;
   constexpr size_t STG = 4 * 32 * BN * sizeof(TOut);
   constexpr int MAXS = static_cast<int>((227 * 1024 - 2048 - STG) / STAGE);
   static_assert(MAXS >= 2, "gemm_tc tile does not fit shared memory");
-  const int nk = (a.K + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T));
-  if (MAXS >= 8 && nk > 8)
-    run<T, TOut, BN, 8>(a, st);
-  else if (MAXS >= 6 && nk > 4)
-    run<T, TOut, BN, 6>(a, st);
-  else if (MAXS >= 4)
-    run<T, TOut, BN, 4>(a, st);
-  else if (MAXS >= 3)
-    run<T, TOut, BN, 3>(a, st);
+  const int stages = std::min(MAXS, gemm_tc_stages(a));
+  if (stages >= 8)
+    run<T, TOut, BN, 8>(a, m, st);
+  else if (stages >= 6)
+    run<T, TOut, BN, 6>(a, m, st);
+  else if (stages >= 4)
+    run<T, TOut, BN, 4>(a, m, st);
+  else if (stages >= 3)
+    run<T, TOut, BN, 3>(a, m, st);
   else
-    run<T, TOut, BN, 2>(a, st);
+    run<T, TOut, BN, 2>(a, m, st);
 }
 
 }  // namespace
@@ -430,43 +341,48 @@ bool gemm_tc_supported(int M, int N, int K, int elem_bytes) {
          (static_cast<int64_t>(N) * elem_bytes) % 16 == 0;
 }
 
-void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaStream_t st) {
+int gemm_tc_max_stages(int BN, bool bf16) {
+  const size_t stage = 128 * 128 + static_cast<size_t>(BN) * 128;
+  const size_t stg = 4 * 32 * static_cast<size_t>(BN) * (bf16 ? 2 : 4);
+  return static_cast<int>((227 * 1024 - 2048 - stg) / stage);
+}
+
+int gemm_tc_stages(const GemmTcArgs& a) { return std::max(2, std::min(a.stages, 8)); }
+
+void gemm_tc_maps(const GemmTcArgs& a, const void* A, const void* B, void* C, GemmTcMaps& m) {
   const int es = a.bf16 ? 2 : 4;
   const uint32_t bk = 128 / es;
-  if (A != a.last_A || B != a.last_B) {
-    const uint64_t da[3] = {static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.M),
-                            static_cast<uint64_t>(a.a_shared ? 1 : a.batch)};
-    const uint64_t sa[2] = {static_cast<uint64_t>(a.K) * es, static_cast<uint64_t>(a.K) * a.M * es};
-    const uint32_t ba[3] = {bk, 128, 1};
-    encode_map(&a.mapA, a.bf16, !a.bf16, A, 3, da, sa, ba);
-    if (a.cs > 1) {  // multicast slices: 128/cs rows per CTA of the cluster
-      const uint32_t bam[3] = {bk, static_cast<uint32_t>(128 / a.cs), 1};
-      encode_map(&a.mapAm, a.bf16, !a.bf16, A, 3, da, sa, bam);
-    }
-    const uint64_t db[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.batch)};
-    const uint64_t sb[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.K * es};
-    const uint32_t bb[3] = {bk, bk, 1};  // 128 B of N x BK rows of K
-    encode_map(&a.mapB, a.bf16, !a.bf16, B, 3, db, sb, bb, /*atom32=*/!a.bf16);
-    a.last_A = A;
-    a.last_B = B;
+  const uint64_t da[3] = {static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.M),
+                          static_cast<uint64_t>(a.a_shared ? 1 : a.batch)};
+  const uint64_t sa[2] = {static_cast<uint64_t>(a.K) * es, static_cast<uint64_t>(a.K) * a.M * es};
+  const uint32_t ba[3] = {bk, 128, 1};
+  encode_map(&m.A, a.bf16, !a.bf16, A, 3, da, sa, ba);
+  if (a.cs > 1) {  // multicast slices: 128/cs rows per CTA of the cluster
+    const uint32_t bam[3] = {bk, static_cast<uint32_t>(128 / a.cs), 1};
+    encode_map(&m.Am, a.bf16, !a.bf16, A, 3, da, sa, bam);
   }
-  if (C != a.C) {  // output map: 128 B column blocks x 32 rows (one epilogue warp's slice)
-    const uint64_t dc[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.batch)};
-    const uint64_t sc[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.M * es};
-    const uint32_t bc[3] = {static_cast<uint32_t>(128 / es), 32, 1};
-    encode_map(&a.mapC, a.bf16, false, C, 3, dc, sc, bc);
-    a.C = C;
-  }
+  const uint64_t db[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.batch)};
+  const uint64_t sb[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.K * es};
+  const uint32_t bb[3] = {bk, bk, 1};  // 128 B of N x BK rows of K
+  encode_map(&m.B, a.bf16, !a.bf16, B, 3, db, sb, bb, /*atom32=*/!a.bf16);
+  // output map: 128 B column blocks x 32 rows (one epilogue warp's slice)
+  const uint64_t dc[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.batch)};
+  const uint64_t sc[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.M * es};
+  const uint32_t bc[3] = {static_cast<uint32_t>(128 / es), 32, 1};
+  encode_map(&m.C, a.bf16, false, C, 3, dc, sc, bc);
+}
+
+void launch_gemm_tc(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   if (a.bf16) {
     switch (a.BN) {
-      case 64: run_bn<__nv_bfloat16, __nv_bfloat16, 64>(a, st); break;
-      case 128: run_bn<__nv_bfloat16, __nv_bfloat16, 128>(a, st); break;
-      default: run_bn<__nv_bfloat16, __nv_bfloat16, 256>(a, st); break;
+      case 64: run_bn<__nv_bfloat16, __nv_bfloat16, 64>(a, m, st); break;
+      case 128: run_bn<__nv_bfloat16, __nv_bfloat16, 128>(a, m, st); break;
+      default: run_bn<__nv_bfloat16, __nv_bfloat16, 256>(a, m, st); break;
     }
   } else {
     switch (a.BN) {
-      case 64: run_bn<float, float, 64>(a, st); break;
-      default: run_bn<float, float, 128>(a, st); break;
+      case 64: run_bn<float, float, 64>(a, m, st); break;
+      default: run_bn<float, float, 128>(a, m, st); break;
     }
   }
 }

@@ -31,58 +31,61 @@ void encode_map_swizzle(CUtensorMap* map, bool bf16, bool tf32, const void* ptr,
                         const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle);
 
 // ---- tensor-core GEMM family (gemm_tc.cu) ----
+// The plan is immutable after prepare; tensor maps over the caller's buffers are built per
+// (A, B, C) by gemm_tc_maps and passed to the launch (the kernel handle caches them).
 struct GemmTcArgs {
-  CUtensorMap mapA, mapB, mapC;  // rebuilt when the operand / output pointers change
-  CUtensorMap mapAm;             // A slices for cluster multicast (box rows 128 / cs)
-  const void* last_A = nullptr;
-  const void* last_B = nullptr;
-  void* C = nullptr;
   int M = 0, N = 0, K = 0, batch = 1, BN = 128;
-  int cs = 1;  // cluster size along N (A multicast), 1 = no cluster
-  int splits = 1;                         // split-K factor (fp32 output only)
-  float* partials = nullptr;              // (splits-1) partial tiles per output tile
-  unsigned long long* flags = nullptr;    // per-tile partner counters (zeroed at prepare)
-  unsigned long long flag_target = 0;     // counter value the owners wait for in the last launch
+  int stages = 4;  // smem ring depth (from the schedule's level-1 k tile)
+  int cs = 1;      // cluster size along N (A multicast), 1 = no cluster
   int sms = 148;
   bool bf16 = false;
   bool a_shared = false;  // A is one matrix for every batch entry (1x1 conv: the filter bank)
 };
+struct GemmTcMaps {
+  CUtensorMap A, B, C, Am;  // Am: A slices for cluster multicast (box rows 128 / cs)
+};
 bool gemm_tc_supported(int M, int N, int K, int elem_bytes);
-void launch_gemm_tc(GemmTcArgs& a, const void* A, const void* B, void* C, cudaStream_t st);
+int gemm_tc_max_stages(int BN, bool bf16);
+int gemm_tc_stages(const GemmTcArgs& a);
+void gemm_tc_maps(const GemmTcArgs& a, const void* A, const void* B, void* C, GemmTcMaps& m);
+void launch_gemm_tc(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st);
 
 // ---- tensor-core implicit-GEMM conv2d family (conv_tc.cu) ----
+// Workspace (caller- or per-stream-owned, conv_tc_ws_bytes): the converted filter bank W' and the
+// NHWC copy of the input, both rewritten by the pre-pass launch of every execute.
 struct ConvTcArgs {
-  CUtensorMap mapW;   // over the W'[r][s][f][c] workspace, built once
-  CUtensorMap mapX;   // over the NHWC copy, dimensions permuted to (c, w, n, h)
-  bool maps_ready = false;
-  void* ws_w = nullptr;  // W' workspace, rewritten by the pre-pass launch of every execute
-  void* ws_x = nullptr;  // NHWC copy of the input, rewritten by the pre-pass launch
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
   int sms = 148;
   bool bf16 = false;
-  bool ns = false;  // conv_ns: filter columns folded into the UMMA N (4 x 32 position tiles)
+  bool ns = false;   // conv_ns: filter columns folded into the UMMA N (4 x 32 position tiles)
   bool s2d = false;  // conv_ns over the space-to-depth form of a stride-2 conv (ResNet stem)
-  CUtensorMap mapO;  // conv_ns: the NCHW output as (w, h, f, n) for TMA stores
-  const void* last_O = nullptr;
+  size_t w_off = 0, x_off = 0, ws_bytes = 0;  // workspace layout: W' at w_off, X at x_off
 };
+struct ConvTcMaps {
+  CUtensorMap W;  // over W' in the workspace
+  CUtensorMap X;  // over the NHWC copy (conv_tc: dims permuted to (c, w, n, h))
+  CUtensorMap O;  // conv_ns: the NCHW output as (w, h, f, n) for TMA stores
+};
+void conv_tc_maps(const ConvTcArgs& a, void* ws, void* O, ConvTcMaps& m);
 // ---- general tensor-core implicit-GEMM conv2d reading NCHW in place (conv_gemm.cu) ----
 struct ConvGemmArgs {
-  CUtensorMap mapW;  // over W'[r][s][f][Cp]
-  bool map_ready = false;
-  void* ws_w = nullptr;  // W' workspace (pre-pass launch of every execute)
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, stride = 1, OH = 0, OW = 0;
   int BN = 128;
   int packed = 0;  // few channels: the (s, c) pairs of a filter row form one K axis
   int sms = 148;
+  size_t ws_bytes = 0;  // W'[r][s][f][Cp] (pre-pass launch of every execute)
 };
-void launch_conv_gemm(ConvGemmArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
+void conv_gemm_map(const ConvGemmArgs& a, void* ws, CUtensorMap& mapW);
+void launch_conv_gemm(const ConvGemmArgs& a, const CUtensorMap& mapW, const void* I, const void* K, void* O,
+                      void* ws, cudaStream_t st, Marks& mk);
 
 bool conv_tc_supported(int C, int F, int R, int S, int stride, bool bf16);
 bool conv_tc_prepass_fits(int C, int W);
 bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16);
 bool conv_s2d_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
-void launch_conv_tc(ConvTcArgs& a, const void* I, const void* K, void* O, cudaStream_t st, Marks& mk);
+void launch_conv_tc(const ConvTcArgs& a, const ConvTcMaps& m, const void* I, const void* K, void* O, void* ws,
+                    cudaStream_t st, Marks& mk);
 
 // ---- HBM-streaming family (stream.cu): gemv / softmax / avgpool2d / dwconv2d ----
 enum class StreamKind : int { Gemv, Softmax, AvgPool, DwConv };

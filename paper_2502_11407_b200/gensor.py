@@ -96,6 +96,8 @@ def _load() -> ctypes.CDLL:
         "gensor_kernel_info": (I, [P, ctypes.c_char_p, SZ, SZP]),
         "gensor_execute": (I, [P, PP, I, P, P]),
         "gensor_execute_host": (I, [P, PP, I, P, P]),
+        "gensor_kernel_workspace_size": (I, [P, SZP]),
+        "gensor_execute_ws": (I, [P, PP, I, P, P, SZ, P]),
         "gensor_kernel_free": (None, [P]),
         "gensor_launch_count": (ctypes.c_uint64, []),
         "gensor_kernel_set_timing": (I, [P, I]),
@@ -120,6 +122,7 @@ EXPORTED = [
     "gensor_candidates", "gensor_caching_benefit", "gensor_vthread_conflict_ratio",
     "gensor_anneal_cache_multiplier", "gensor_record_probability", "gensor_derive_seed",
     "gensor_kernel_prepare", "gensor_kernel_info", "gensor_execute", "gensor_execute_host",
+    "gensor_kernel_workspace_size", "gensor_execute_ws",
     "gensor_kernel_free", "gensor_launch_count", "gensor_kernel_set_timing", "gensor_kernel_timings",
     "gensor_rerank", "gensor_emit_source", "gensor_analyze",
 ]
@@ -401,15 +404,31 @@ class Kernel:
         """Plan, variant, work and (after the first host-buffer execute) the copy pipeline."""
         return _json_call(_lib.gensor_kernel_info, self._h)
 
-    def execute(self, inputs: Sequence[Any], output: Any, stream: Any = None) -> None:
+    @property
+    def workspace_bytes(self) -> int:
+        """Device workspace one execute needs (0 for families without a pre-pass)."""
+        n = ctypes.c_size_t(0)
+        _check(_lib.gensor_kernel_workspace_size(self._h, ctypes.byref(n)))
+        return n.value
+
+    def execute(self, inputs: Sequence[Any], output: Any, stream: Any = None, workspace: Any = None) -> None:
         """Device execute: ``inputs``/``output`` are CUDA tensors (or raw device pointers);
-        asynchronous on ``stream`` (torch.cuda.Stream, raw handle, or None = current stream)."""
+        asynchronous on ``stream`` (torch.cuda.Stream, raw handle, or None = current stream).
+        ``workspace``: an optional caller-owned device buffer of ``workspace_bytes`` bytes
+        (gensor_execute_ws); by default the handle keeps one per stream."""
+        _check_tensors(self.op, inputs, output, device=True)
         ptrs = (ctypes.c_void_p * max(1, len(inputs)))(*[_ptr(t) for t in inputs])
-        _check(_lib.gensor_execute(self._h, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
-                                   ctypes.c_void_p(_stream(stream))))
+        if workspace is None:
+            _check(_lib.gensor_execute(self._h, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
+                                       ctypes.c_void_p(_stream(stream))))
+        else:
+            nbytes = workspace.numel() * workspace.element_size() if hasattr(workspace, "numel") else self.workspace_bytes
+            _check(_lib.gensor_execute_ws(self._h, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
+                                          ctypes.c_void_p(_ptr(workspace)), nbytes, ctypes.c_void_p(_stream(stream))))
 
     def execute_host(self, inputs: Sequence[Any], output: Any, stream: Any = None) -> None:
         """Host-buffer execute (the interpreter's convention): copies in, runs, copies out, syncs."""
+        _check_tensors(self.op, inputs, output, device=False)
         ptrs = (ctypes.c_void_p * max(1, len(inputs)))(*[_ptr(t) for t in inputs])
         _check(_lib.gensor_execute_host(self._h, ptrs, len(inputs), ctypes.c_void_p(_ptr(output)),
                                         ctypes.c_void_p(_stream(stream))))
@@ -429,6 +448,47 @@ class Kernel:
         if getattr(self, "_h", None) and self._h.value:
             _lib.gensor_kernel_free(self._h)
             self._h = None
+
+
+def _tensor_elems(op: "TensorOpSpec", i: int) -> int:
+    n = 1
+    for d in op.tensors[i]["true_dims"]:
+        n *= d
+    return n * op.batch
+
+
+def _check_tensors(op: "TensorOpSpec", inputs: Sequence[Any], output: Any, device: bool) -> None:
+    """Argument checks of the Python mirror: tensor arguments must match the op's tensors in
+    element count, dtype (fp32 for dtype_bytes 4, bf16 for 2), contiguity and device. Raw integer
+    pointers pass through unchecked (explicit pointer use)."""
+    want = {4: ("float32",), 2: ("bfloat16",)}.get(op.dtype_bytes, ())
+    args = list(inputs) + [output]
+    if len(inputs) != len(op.tensors) - 1:
+        return  # the library reports ShapeMismatch
+    for i, t in enumerate(args):
+        if isinstance(t, int):
+            continue
+        name = op.tensors[i].get("name", str(i)) if isinstance(op.tensors[i], dict) else str(i)
+        if hasattr(t, "is_cuda"):  # torch tensor
+            if t.is_cuda != device:
+                raise ValueError(f"tensor {name}: expected a {'CUDA' if device else 'host'} tensor")
+            if not t.is_contiguous():
+                raise ValueError(f"tensor {name}: must be contiguous")
+            dt = str(t.dtype).replace("torch.", "")
+        elif hasattr(t, "ctypes"):  # numpy array (host buffers only)
+            if device:
+                raise ValueError(f"tensor {name}: a numpy array is a host buffer; execute needs device memory")
+            if not t.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"tensor {name}: must be C-contiguous")
+            dt = "bfloat16" if (t.dtype.itemsize == 2 and op.dtype_bytes == 2) else str(t.dtype)
+        else:
+            continue
+        if want and dt not in want:
+            raise ValueError(f"tensor {name}: dtype {dt}, the op stores {want[0]} (dtype_bytes {op.dtype_bytes})")
+        n = t.numel() if hasattr(t, "numel") else t.size
+        need = _tensor_elems(op, i)
+        if n < need:
+            raise ValueError(f"tensor {name}: {n} elements, the op needs {need}")
 
 
 def _ptr(t: Any) -> int:

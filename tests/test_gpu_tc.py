@@ -111,12 +111,22 @@ CONVS = [
     {"kind": "conv2d", "I": [1, 48, 10, 70], "K": [128, 48, 3, 1], "S": 1},   # S = 1, F = 128: N = 128
     {"kind": "conv2d", "I": [3, 128, 14, 18], "K": [128, 128, 3, 3], "S": 1},  # filters streamed per stage
     {"kind": "conv2d", "I": [2, 96, 11, 13], "K": [100, 96, 3, 3], "S": 1},   # streamed, ragged F / C
+    {"kind": "conv2d", "I": [2, 3, 16, 18], "K": [32, 3, 3, 3], "S": 1},      # C = 3: no 16 B NHWC rows
 ]
 
 
 @pytest.mark.parametrize("doc", CONVS, ids=lambda d: json.dumps(d["I"] + d["K"]))
 @pytest.mark.parametrize("variant,tol", [("tc_tf32", TF32_TOL), ("tc_bf16", BF16_TOL)])
 def test_conv_tc(doc, variant, tol):
+    C = doc["I"][1]
+    if variant == "tc_bf16" and (C * 2) % 16:
+        # bf16 convs need 16 B channel rows for the NHWC TMA boxes: the family refuses loudly
+        op = g.TensorOpSpec.parse_text(json.dumps(doc))
+        sched = g.optimize(op, hw(), g.EngineConfig(seed=0, mode="b200", top_k=1))
+        with pytest.raises(g.GensorError) as e:
+            g.Kernel(op, sched, 0, variant)
+        assert e.value.code == "Unsupported"
+        return
     info = check(doc, variant, tol)
     # 1x1 tf32 convs take the in-place implicit GEMM (no NHWC pre-pass), windows take conv_tc
     F, S = doc["K"][0], doc["K"][3]
@@ -127,9 +137,9 @@ def test_conv_tc(doc, variant, tol):
     if (variant == "tc_tf32" and doc["K"][2] == 1 and doc["K"][3] == 1 and doc["I"][1] % 4 == 0 and P % 4 == 0
             and (P >= 512 or P % 128 == 0)):
         want = "gemm_tc"    # 1x1 stride 1: batched GEMM O[n] = K . I[n] on the NCHW tensors
-    elif variant == "tc_tf32" and doc["K"][2] == 1:
-        want = "conv_gemm"  # other 1x1: the in-place implicit GEMM
-    elif variant == "tc_tf32" and S <= 4 and S * fn <= 256:
+    elif variant == "tc_tf32" and (doc["K"][2] == 1 or C % 4):
+        want = "conv_gemm"  # other 1x1, and channel counts without 16 B NHWC rows: in-place implicit GEMM
+    elif variant == "tc_tf32" and S <= 4 and S * fn <= 256 and C % 4 == 0:
         want = "conv_ns"    # NCHW in place, filter columns folded into the UMMA N
     else:
         want = "conv_tc"    # NHWC copy + TMA boxes
