@@ -41,7 +41,10 @@ WORKLOADS = {
                    name="Conv2d ResNet-50 layer N=16 56x56x64->64 3x3 stride 1 (implicit GEMM, pre-padded 58x58 input)",
                    bound="tensor", unit="TFLOP/s"),
     "gemm": dict(op={"kind": "gemm", "M": 1024, "K": 1024, "N": 1024},
-                 name="GEMM fp32 M=N=K=1024", bound="tensor", unit="TFLOP/s"),
+                 name="GEMM fp32 M=N=K=1024 (tf32 tensor cores)", bound="tensor", unit="TFLOP/s"),
+    "gemm_fp32": dict(op={"kind": "gemm", "M": 1024, "K": 1024, "N": 1024},
+                      name="GEMM fp32 M=N=K=1024 at fp32 accuracy (3xTF32 tensor cores, 1e-6 bar)",
+                      bound="tensor", unit="TFLOP/s", variant="tc_3xtf32"),
     "bgemm": dict(op={"kind": "gemm", "M": 512, "K": 64, "N": 512, "dtype_bytes": 2, "batch": 192},
                   name="Batched GEMM bf16 B*H=192 512x64x512 (attention QK^T shape)", bound="hbm", unit="TFLOP/s"),
     "rowsum": dict(op={"kind": "gemv", "M": 32768, "N": 4096},
@@ -53,7 +56,7 @@ WORKLOADS = {
     "avgpool": dict(op={"kind": "avgpool2d", "I": [32, 256, 114, 114], "F": 3, "S": 1},
                     name="AvgPool 3x3 s1 fp32 32x256x112x112", bound="hbm", unit="GB/s"),
 }
-SUITE_DEFAULT = ["gemm", "bgemm", "rowsum", "softmax", "dwconv", "avgpool"]
+SUITE_DEFAULT = ["gemm_fp32", "gemm", "bgemm", "rowsum", "softmax", "dwconv", "avgpool"]
 
 # the B200 in the reference's own hardware format (for oracle/_ref).
 B200_REF_HW = {
@@ -219,8 +222,11 @@ def tf32_peak(torch, device) -> float:
     return 2 * 8192 ** 3 / best / 1e12
 
 
-def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None, e2e=True, timing=True, seed=0):
-    """Construct + instantiate + time one op. Returns a dict of measurements (this rank)."""
+def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None, e2e=True, timing=True, seed=0,
+           rerank=True):
+    """Construct + instantiate + time one op. Returns a dict of measurements (this rank).
+    rerank: the paper's flow — the engine's top-k schedules are instantiated and timed on the
+    device (gensor_rerank) and the fastest one is the kernel; its time is reported apart."""
     op = g.TensorOpSpec.parse_text(json.dumps(spec["op"]))
     cfg = g.EngineConfig(seed=0, mode="b200")
     con = []
@@ -229,11 +235,17 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
         t0 = time.perf_counter()
         sched = g.optimize(op, hw, cfg)
         con.append(time.perf_counter() - t0)
-    k = g.Kernel(op, sched, 0, variant)
     rng = torch.Generator(device=device)
     rng.manual_seed(seed)
     xs, out = make_inputs(op, spec, rng, torch, device)
     stream = torch.cuda.current_stream(device)
+    best, rr, rerank_s = 0, None, None
+    if rerank and len(sched) > 1:
+        t0 = time.perf_counter()
+        rr = g.rerank(op, sched, xs, out, variant, iters=5, stream=stream)
+        rerank_s = time.perf_counter() - t0
+        best = rr["best"]
+    k = g.Kernel(op, sched, best, variant)
     for _ in range(warmup):
         k.execute(xs, out, stream)
     torch.cuda.synchronize(device)
@@ -262,7 +274,9 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
                 launch_ms.setdefault(name, []).append(ms)
         k.set_timing(False)
     res = dict(op=op, kernel=k, sched=sched, step_ms=step_ms, launch_ms=launch_ms, launches=launches,
-               construct_s=statistics.median(con), flops=op.flops, bytes=op.bytes)
+               construct_s=statistics.median(con), flops=op.flops, bytes=op.bytes, index=best,
+               rerank=None if rr is None else {"ms": rr["ms"], "best": best, "wall_s": rerank_s,
+                                               "plans_differ": len({json.dumps(p) for p in rr.get("plans", [])}) > 1})
     if e2e:
         hin = [x.cpu().pin_memory() for x in xs]
         hout = torch.empty(out.numel(), dtype=out.dtype).pin_memory()
@@ -292,6 +306,8 @@ def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=None):
         achieved = res["flops"] / avg / 1e12
         if variant_name == "tc_tf32":
             peak, src = tf32_tflops, "cuBLAS tf32 8192^3 measured in this run (best of 5)"
+        elif variant_name == "tc_3xtf32":  # three tf32 MMAs per fp32 product
+            peak, src = tf32_tflops / 3, "cuBLAS tf32 8192^3 measured in this run / 3 (3 MMAs per product)"
         else:
             peak, src = peaks["bf16_tflops"], f"bf16 dense, {peaks['source']}"
         r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -649,8 +665,9 @@ def run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, 
         pg.destroy_process_group()
 
 
-GRAPH_VS_TREE = {  # schedule-driven SIMT family: the construction decides the kernel's tiling
+GRAPH_VS_TREE = {  # the families `auto` runs: tensor cores for G / B / C, the HBM family for V / P
     "gemm": {"kind": "gemm", "M": 1024, "K": 1024, "N": 1024},
+    "bgemm": {"kind": "gemm", "M": 512, "K": 64, "N": 512, "dtype_bytes": 2, "batch": 192},
     "conv2d": {"kind": "conv2d", "I": [16, 64, 58, 58], "K": [64, 64, 3, 3], "S": 1},
     "gemv": {"kind": "gemv", "M": 32768, "N": 4096},
     "avgpool2d": {"kind": "avgpool2d", "I": [32, 256, 114, 114], "F": 3, "S": 1},
@@ -659,10 +676,12 @@ GRAPH_VS_TREE = {  # schedule-driven SIMT family: the construction decides the k
 
 def run_graph_vs_tree(args, g, torch, hw, flush, device):
     """SURVEY.md §8f rank 2 / the paper's core claim (graph construction >= tree construction,
-    PAPER.md:577): the same state-driven SIMT kernel family instantiated from the
-    graph-constructed schedule (optimize, B200 mode), from the on-device re-ranked top-k of the
-    graph, and from the Roller-style tree schedule (construct_tree, B200 mode), timed on B200."""
+    PAPER.md:577): the kernel `auto` runs (tcgen05 for the GEMMs and the conv, the
+    HBM-streaming family for the row / window ops) instantiated from the graph-constructed
+    schedule (optimize, B200 mode), from the on-device re-ranked top-k of the graph, and from the
+    Roller-style tree schedule (construct_tree, B200 mode), timed on B200."""
     out = {}
+    variant = getattr(args, "variant", "auto")
     for name, doc in GRAPH_VS_TREE.items():
         op = g.TensorOpSpec.parse_text(json.dumps(doc))
         gen = torch.Generator(device=device)
@@ -672,11 +691,11 @@ def run_graph_vs_tree(args, g, torch, hw, flush, device):
         tree = g.construct_tree(op, hw, 4, "b200")
 
         def timed(sched, idx):
-            k = g.Kernel(op, sched, idx, "simt_f32")
-            for _ in range(2):
+            k = g.Kernel(op, sched, idx, variant)
+            for _ in range(3):
                 k.execute(xs, o)
             ts = []
-            for _ in range(max(3, args.steps)):
+            for _ in range(max(5, args.steps)):
                 flush.zero_()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
@@ -684,27 +703,35 @@ def run_graph_vs_tree(args, g, torch, hw, flush, device):
                 e.record()
                 e.synchronize()
                 ts.append(s.elapsed_time(e))
-            return statistics.median(ts)
+            return statistics.median(ts), k.info["plan"]
 
-        t_graph = timed(graph, 0)
-        rr = g.rerank(op, graph, xs, o, "simt_f32", iters=3)
-        t_rerank = timed(graph, rr["best"])
-        t_tree = timed(tree, 0)
+        t_graph, p_graph = timed(graph, 0)
+        rr = g.rerank(op, graph, xs, o, variant, iters=5)
+        t_rerank, p_rerank = timed(graph, rr["best"])
+        t_tree, p_tree = timed(tree, 0)
         unit_work = op.flops if doc["kind"] in ("gemm", "conv2d") else op.bytes
         scale, unit = (1e12, "TFLOP/s") if doc["kind"] in ("gemm", "conv2d") else (1e9, "GB/s")
+        distinct = sorted({json.dumps(p, sort_keys=True) for p in rr["plans"] if p})
         out[name] = {"unit": unit,
                      "graph": {"ms": t_graph, "value": unit_work / (t_graph / 1e3) / scale,
-                               "schedule": graph[0]["state"]["repr"]},
+                               "schedule": graph[0]["state"]["repr"], "plan": p_graph,
+                               "est_ms": graph[0]["cost"]["est_seconds"] * 1e3},
                      "graph_reranked": {"ms": t_rerank, "value": unit_work / (t_rerank / 1e3) / scale,
-                                        "schedule": graph[rr["best"]]["state"]["repr"], "index": rr["best"]},
+                                        "schedule": graph[rr["best"]]["state"]["repr"], "index": rr["best"],
+                                        "plan": p_rerank},
                      "tree": {"ms": t_tree, "value": unit_work / (t_tree / 1e3) / scale,
-                              "schedule": tree[0]["state"]["repr"]},
-                     "graph_over_tree": t_tree / t_graph}
+                              "schedule": tree[0]["state"]["repr"], "plan": p_tree,
+                              "est_ms": tree[0]["cost"]["est_seconds"] * 1e3},
+                     "topk_rerank_ms": rr["ms"], "topk_distinct_plans": len(distinct),
+                     "graph_over_tree": t_tree / t_graph, "reranked_over_tree": t_tree / t_rerank}
     geo = float(np.exp(np.mean([np.log(v["graph_over_tree"]) for v in out.values()])))
-    line = {"metric": "graph vs tree construction: measured B200 time of the SIMT family (speed-up)",
-            "value": geo, "unit": "x (geomean tree time / graph time)", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic U(-1,1)", "config": {"workload": "graph_vs_tree"},
+    geo_rr = float(np.exp(np.mean([np.log(v["reranked_over_tree"]) for v in out.values()])))
+    line = {"metric": "graph vs tree construction: measured B200 time of the kernel auto runs (speed-up)",
+            "value": geo, "unit": "x (geomean tree time / graph time)", "reranked_geomean": geo_rr,
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "per op (tf32 / bf16 / f32)", "data": "synthetic U(-1,1)",
+            "config": {"workload": "graph_vs_tree", "variant": variant,
+                       "l2": "flushed between steps (256 MiB write outside the events)"},
             "per_op": out}
     print(json.dumps(line), flush=True)
 
@@ -789,18 +816,17 @@ def run_ours(args):
             if not wname or wname == args.workload:
                 continue
             try:
-                r = run_op(g, torch, WORKLOADS[wname], hw, max(5, args.steps), max(3, args.warmup), device, "auto",
-                           flush, e2e=False)
-                ki = r["kernel"].info
                 sp = WORKLOADS[wname]
+                r = run_op(g, torch, sp, hw, max(5, args.steps), max(3, args.warmup), device,
+                           sp.get("variant", "auto"), flush, e2e=False)
+                ki = r["kernel"].info
                 w = r["flops"] if sp["unit"] == "TFLOP/s" else r["bytes"]
+                rl = roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname))
                 suite[wname] = {
-                    "op": sp["op"], "variant": ki["variant_name"], "family": ki["plan"].get("family"),
-                    "schedule": ki["state"]["repr"],
+                    "variant": ki["variant_name"], "family": ki["plan"].get("family"),
                     "value": w / (statistics.mean(r["step_ms"]) / 1e3) / (1e12 if sp["unit"] == "TFLOP/s" else 1e9),
                     "unit": sp["unit"], "ms_per_step": statistics.mean(r["step_ms"]),
-                    "roofline": roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname)),
-                    "launch_breakdown_ms": {n: statistics.mean(v) for n, v in r["launch_ms"].items()},
+                    "roofline": {k: rl[k] for k in ("bound", "achieved", "peak", "frac", "traffic", "kernel")},
                     "construction_s": r["construct_s"],
                 }
                 del r
@@ -811,7 +837,7 @@ def run_ours(args):
     base = None
     ref_con = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(spec, res["sched"][0]["state"], budget_s=args.ref_budget)
+        base = cpu_baseline(spec, res["sched"][res["index"]]["state"], budget_s=args.ref_budget)
         ref_con = reference_construct_s(spec)
 
     if rank != 0:
@@ -823,6 +849,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": glob["scaling"],
         "vs_baseline": None,
         "dtype": {"tc_tf32": "tf32 (fp32 storage, fp32 accumulate)", "tc_bf16": "bf16 (fp32 accumulate)",
+                  "tc_3xtf32": "fp32-grade 3xTF32 (fp32 storage, fp32 accumulate)",
                   "simt_f32": "f32", "simt_parity": "f64 accumulate", "stream": "f32"}[info["variant_name"]],
         "data": "synthetic U(-1,1)",
         "config": {"workload": spec["name"], "op": spec["op"], "variant": info["variant_name"],
@@ -839,6 +866,7 @@ def run_ours(args):
         "gpu_launches": res["launches"],
         "launch_breakdown_ms": {n: statistics.mean(v) for n, v in res["launch_ms"].items()},
         "construction_s": res["construct_s"],
+        "schedule_index": res["index"], "rerank": res["rerank"],
         "construction_reference_s": ref_con,
         "clocks": clk.summary(),
         "cpu_baseline": base,

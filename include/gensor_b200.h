@@ -65,8 +65,11 @@ enum gensor_variant {
   GENSOR_VARIANT_SIMT_F32 = 1,     /* state-driven SIMT kernel, fp32 FFMA accumulation */
   GENSOR_VARIANT_TC_TF32 = 2,      /* tcgen05 kind::tf32, TMEM accumulator (gemm, conv2d) */
   GENSOR_VARIANT_TC_BF16 = 3,      /* tcgen05 kind::f16 bf16 operands (gemm, conv2d) */
-  GENSOR_VARIANT_STREAM = 4        /* HBM-streaming families: gemv/row-sum, softmax, pooling,
+  GENSOR_VARIANT_STREAM = 4,       /* HBM-streaming families: gemv/row-sum, softmax, pooling,
                                       depthwise conv (128-bit loads, warp shuffles) */
+  GENSOR_VARIANT_TC_3XTF32 = 5     /* fp32-grade tcgen05 GEMM: each fp32 operand split into
+                                      tf32 hi + lo in shared memory, 3 MMAs per k-step (~fp32
+                                      accuracy, the SPEC's 1e-6 single-precision bar) */
 };
 
 enum gensor_mode {
@@ -188,7 +191,8 @@ void gensor_kernel_free(gensor_kernel* k);
 /* On-device re-ranking of the constructed top-k (the paper profiles its top
  * candidates on hardware, the reference ranks by the analytical estimate_cost only, engine.cpp:
  * 179-190): instantiates every complete result of `s` with `variant`, times `iters` executes on
- * the caller's device buffers and writes {"ms":[...],"order":[...],"best":i} (fastest first). */
+ * the caller's device buffers and writes {"ms":[...],"order":[...],"best":i,"plans":[...]} (order:
+ * fastest first; plans: the kernel plan each result instantiates). */
 int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, const void* const* d_inputs,
                   int n_inputs, void* d_output, void* stream, int iters, char* buf, size_t cap, size_t* need);
 

@@ -501,6 +501,7 @@ int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, co
   return guarded([&]() -> int {
     check_schedule_op(op->op, *s);
     std::vector<std::pair<float, int>> t;
+    std::vector<std::string> plans;
     std::ostringstream os;
     os << "{\"ms\":[";
     for (size_t i = 0; i < s->results.size(); ++i) {
@@ -508,6 +509,7 @@ int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, co
       float ms = -1.f;
       if (st.complete()) {
         gb::dev::Kernel* k = gb::dev::prepare(op->op, st, variant);
+        plans.push_back(gb::dev::plan(k));
         try {
           ms = gb::dev::time_execute(k, d_in, n_in, d_out, stream, iters);
         } catch (...) {
@@ -516,13 +518,17 @@ int gensor_rerank(const gensor_op* op, const gensor_schedule* s, int variant, co
         }
         gb::dev::destroy(k);
         t.emplace_back(ms, static_cast<int>(i));
+      } else {
+        plans.push_back("null");
       }
       os << (i ? "," : "") << gb::json::num(ms);
     }
     std::stable_sort(t.begin(), t.end());  // ties keep the analytical order
     os << "],\"order\":[";
     for (size_t i = 0; i < t.size(); ++i) os << (i ? "," : "") << t[i].second;
-    os << "],\"best\":" << (t.empty() ? -1 : t[0].second) << "}";
+    os << "],\"best\":" << (t.empty() ? -1 : t[0].second) << ",\"plans\":[";
+    for (size_t i = 0; i < plans.size(); ++i) os << (i ? "," : "") << plans[i];
+    os << "]}";
     return emit(os.str(), buf, cap, need);
   });
 }

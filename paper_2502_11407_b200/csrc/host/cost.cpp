@@ -6,6 +6,7 @@
 
 #include "error.hpp"
 #include "json.hpp"
+#include "tcplan.hpp"
 
 namespace gb {
 
@@ -144,6 +145,24 @@ Cost estimate(const OpDesc& op, const HwModel& hw, const Sched& s) {
 Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s) {
   Cost c = estimate(op, hw, s);
   const DeviceLimits& d = hw.dev;
+  const ExecUnit unit = exec_unit(op);
+  const double hbm_floor = op.bytes_true() / d.hbm_bytes_per_s;
+  if (op.kind == Kind::Gemm && tensor_unit(unit)) {
+    // the tensor-core program this state instantiates (UMMA tile, ring depth from the level-1 tile)
+    const bool bf16 = unit == ExecUnit::TensorBf16;
+    const GemmTcPlan p = gemm_tc_plan(op, s, bf16, false);
+    const int64_t M = op.param("M"), N = op.param("N"), K = op.param("K");
+    const double t = gemm_tc_seconds(d, M, N, K, op.batch, op.dtype_bytes, op.dtype_bytes, p,
+                                     bf16 ? d.bf16_tc_flops : d.tf32_tc_flops);
+    const double tiles = static_cast<double>(((M + p.BM - 1) / p.BM) * ((N + p.BN - 1) / p.BN) * op.batch);
+    c.waves = std::ceil(tiles / (d.sms / p.cs * p.cs));
+    c.occupancy = tiles / (c.waves * d.sms);
+    c.compute_seconds = t;
+    c.est_seconds = std::max(t, hbm_floor + kLaunchSeconds);
+    c.bottleneck = t >= hbm_floor + kLaunchSeconds ? -1 : 0;
+    c.exec_seconds = c.est_seconds;
+    return c;
+  }
   const int L = std::max(1, s.L);
   double ctas = static_cast<double>(op.batch);
   int64_t threads = 1, acc = 1;
@@ -178,11 +197,18 @@ Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s) {
       c.bottleneck = static_cast<int>(i);
     }
   // HBM floor on true bytes (every byte once), independent of tiling
-  const double hbm = op.bytes_true() / d.hbm_bytes_per_s;
-  if (hbm > c.est_seconds) {
-    c.est_seconds = hbm;
+  if (hbm_floor > c.est_seconds) {
+    c.est_seconds = hbm_floor;
     c.bottleneck = 0;
   }
+  // the family `auto` runs: tensor-core conv (fixed-shape plans, state-independent), the
+  // HBM-streaming family (bandwidth-bound), or this SIMT estimate
+  if (op.kind == Kind::Conv2d && tensor_unit(unit))
+    c.exec_seconds = conv_tc_seconds(op, d);
+  else if (unit == ExecUnit::Hbm)
+    c.exec_seconds = hbm_floor + kLaunchSeconds;
+  else
+    c.exec_seconds = c.est_seconds + kLaunchSeconds;
   return c;
 }
 
@@ -194,7 +220,9 @@ std::string cost_json(const Cost& c, const HwModel& hw) {
     os << (i ? "," : "") << "[" << json::quote(hw.levels[i].name) << "," << json::num(c.memory_seconds[i]) << "]";
   os << "],\"bottleneck\":"
      << json::quote(c.bottleneck < 0 ? std::string("compute") : hw.levels[static_cast<size_t>(c.bottleneck)].name);
-  if (hw.is_b200) os << ",\"waves\":" << json::num(c.waves) << ",\"occupancy\":" << json::num(c.occupancy);
+  if (hw.is_b200)
+    os << ",\"waves\":" << json::num(c.waves) << ",\"occupancy\":" << json::num(c.occupancy)
+       << ",\"exec_seconds\":" << json::num(c.exec_seconds);
   os << "}";
   return os.str();
 }

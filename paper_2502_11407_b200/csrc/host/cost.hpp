@@ -24,6 +24,7 @@ struct Cost {
   int bottleneck = -1;                 // -1 = compute, else the source level index
   double waves = 0.0;                  // B200 mode only: CTA waves over the SMs
   double occupancy = 0.0;              // B200 mode only: fraction of the last wave's SM slots used
+  double exec_seconds = 0.0;           // B200 mode only: predicted time of the `auto` kernel family
 };
 
 int64_t footprint_elems(const OpDesc& op, const Sched& s, int level);
@@ -44,8 +45,10 @@ double utilization(const OpDesc& op, const HwModel& hw, const Sched& s);
 // Reference-compatible estimate (cost_model.cpp:179-211). Throws IncompleteState.
 Cost estimate(const OpDesc& op, const HwModel& hw, const Sched& s);
 
-// B200 estimate: the reference terms with the compute channel scaled by wave quantisation,
-// SM occupancy and the variant's peak.
+// B200 estimate. GEMMs that run on the tensor cores are priced as the
+// gemm_tc program the state instantiates (tcplan.hpp); other ops keep the reference terms with the
+// compute channel scaled by wave quantisation, SM occupancy and the execution unit's peak.
+// exec_seconds = the predicted time of the kernel family `auto` runs (the LPT weight).
 Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s);
 
 std::string cost_json(const Cost& c, const HwModel& hw);

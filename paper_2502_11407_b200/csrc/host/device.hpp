@@ -19,6 +19,7 @@ struct Kernel;  // opaque: the instantiated plan + device workspace
 Kernel* prepare(const OpDesc& op, const Sched& s, int variant);  // throws gb::Error
 void destroy(Kernel* k);
 std::string info(const Kernel* k);
+std::string plan(const Kernel* k);  // the instantiated plan (JSON object)
 // ws == nullptr: the handle's workspace for `stream` (allocated on the stream's first execute);
 // otherwise a caller-owned device workspace of ws_size >= workspace_bytes(k) bytes.
 void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, void* ws, size_t ws_size,

@@ -5,6 +5,7 @@
 #include <thread>
 
 #include "error.hpp"
+#include "tcplan.hpp"
 
 namespace gb {
 
@@ -54,10 +55,37 @@ std::vector<int64_t> sorted_unique(std::vector<int64_t> v) {
 //     parallelism term and picks 2-CTA GEMV grids);
 //   level L committed: threads/CTA in [32, max_threads_per_block], per-thread accumulators
 //     (prod of spatial thread tiles) <= 64 so the thread tile lives in registers.
+namespace {
+
+// GEMMs the tensor cores run: their level-1 tile is a gemm_tc program (tcplan.hpp)
+bool tc_gemm(const OpDesc& op) { return op.kind == Kind::Gemm && tensor_unit(exec_unit(op)); }
+
+// K-atom floor of the tensor-core ring: the level-1 k tile holds at least two 128-byte k-blocks.
+// Halving below it can never be undone by completion (it only halves), so B200-mode completion
+// and the tree baseline never take that step.
+bool tc_k_floor_broken(const OpDesc& op, const Sched& s, int level) {
+  return level == 1 && tc_gemm(op) && s.tile(op, 2, 1) * op.dtype_bytes < 256 && op.ax[2].padded * op.dtype_bytes >= 256;
+}
+
+}  // namespace
+
 bool b200_feasible(const OpDesc& op, const HwModel& hw, const Sched& s, int upto_level) {
   if (!hw.is_b200 || s.L < 1) return true;
   const DeviceLimits& d = hw.dev;
-  if (upto_level >= 1) {
+  if (upto_level >= 1 && tc_gemm(op)) {
+    // tensor-core legality of the level-1 tile: UMMA M = 128 rows (cta_group::1), UMMA N within
+    // [16, 256] (fp32 output: <= 128, the epilogue staging shares smem with the ring; TMEM holds
+    // two BN-column accumulators), K ring of >= 2 k-blocks of 128 B (K-atom 32 B). Persistent
+    // CTAs: no wave gate (the cost prices idle SMs).
+    const GemmTcPlan p = gemm_tc_plan(op, s, exec_unit(op) == ExecUnit::TensorBf16, false);
+    const bool short_k = op.ax[2].padded * op.dtype_bytes < 256;  // the whole K is one ring
+    if (!(p.legal || (short_k && s.tile(op, 0, 1) == std::min<int64_t>(128, op.ax[0].padded) &&
+                      s.tile(op, 1, 1) <= gemm_tc_bn_max(exec_unit(op) == ExecUnit::TensorBf16, false))))
+      return false;
+    if (2 * p.BN > d.tmem_cols) return false;
+    // the tile grid fills the SMs when a 64-wide N tile can (the persistent grid is min(tiles, SMs))
+    if (gemm_tc_tiles(op, p.BN) < std::min<int64_t>(d.sms, gemm_tc_tiles(op, 64))) return false;
+  } else if (upto_level >= 1) {
     int64_t ctas = op.batch, max_ctas = op.batch;
     for (int a = 0; a < op.naxes; ++a) {
       if (op.ax[a].reduce) continue;
@@ -179,7 +207,7 @@ std::vector<Result> construct(const OpDesc& op, const HwModel& hw, const EngineC
 
 // Tile(axis, 2) at the editing level whose child moves the least level traffic; ties keep the
 // first axis (strict <), tree_baseline.cpp:13-27.
-bool greedy_fit_step(const OpDesc& op, const Sched& s, Action& out) {
+bool greedy_fit_step(const OpDesc& op, const Sched& s, Action& out, bool tc_floor) {
   if (s.complete()) return false;
   bool found = false;
   int64_t best = 0;
@@ -189,6 +217,7 @@ bool greedy_fit_step(const OpDesc& op, const Sched& s, Action& out) {
     if (!s.legal(op, act)) continue;
     Sched child = s;
     child.apply_unchecked(op, act);
+    if (tc_floor && tc_k_floor_broken(op, child, level)) continue;
     const int64_t q = traffic(op, child, level);
     if (!found || q < best) {
       out = act;
@@ -203,9 +232,29 @@ bool complete(const OpDesc& op, const HwModel& hw, Sched& s, std::vector<Action>
   const bool dev = mode == Mode::B200 && hw.is_b200;
   while (!s.complete()) {
     const int target = s.edit_level();
+    if (dev && target == 1 && tc_gemm(op)) {
+      // shape the level-1 tile into the UMMA range first (M tile 128, N tile <= the epilogue
+      // limit): legal Tile actions recorded in the trace, so the schedule replays
+      const int64_t bn_max = gemm_tc_bn_max(exec_unit(op) == ExecUnit::TensorBf16, false);
+      auto tile_down = [&](int a) {
+        const Action act{ActKind::Tile, a, 2};
+        if (!s.legal(op, act)) return false;
+        s.apply_unchecked(op, act);
+        trace.push_back(act);
+        return true;
+      };
+      while (s.tile(op, 0, 1) > 128 && tile_down(0)) {
+      }
+      while (s.tile(op, 1, 1) > bn_max && tile_down(1)) {
+      }
+      // narrower N tiles while the grid leaves SMs idle (down to UMMA N = 64)
+      const int64_t want = std::min<int64_t>(hw.dev.sms, gemm_tc_tiles(op, 64));
+      while (s.tile(op, 1, 1) > 64 && gemm_tc_tiles(op, s.tile(op, 1, 1)) < want && tile_down(1)) {
+      }
+    }
     while (!capacity_ok(op, hw, s, target) || (dev && !b200_feasible(op, hw, s, target))) {
       Action step;
-      if (!greedy_fit_step(op, s, step)) return false;
+      if (!greedy_fit_step(op, s, step, dev)) return false;
       s.apply_unchecked(op, step);
       trace.push_back(step);
     }
@@ -336,6 +385,7 @@ std::vector<Result> construct_tree(const OpDesc& op, const HwModel& hw, int beam
           if (!b.state.legal(op, act)) continue;
           Beam child{b.state, b.trace, 0};
           child.state.apply_unchecked(op, act);
+          if (dev && tc_k_floor_broken(op, child.state, level)) continue;
           child.trace.push_back(act);
           child.q = traffic(op, child.state, level);
           grown.push_back(std::move(child));

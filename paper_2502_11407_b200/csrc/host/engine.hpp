@@ -71,7 +71,8 @@ std::vector<Result> construct(const OpDesc& op, const HwModel& hw, const EngineC
 
 // Greedy capacity-fitting completion (engine.cpp:149-163); false if some level never fits.
 bool complete(const OpDesc& op, const HwModel& hw, Sched& s, std::vector<Action>& trace, Mode mode);
-bool greedy_fit_step(const OpDesc& op, const Sched& s, Action& out);
+// tc_floor (B200 mode): never halve a tensor-core GEMM's level-1 k tile below two 128 B k-blocks.
+bool greedy_fit_step(const OpDesc& op, const Sched& s, Action& out, bool tc_floor = false);
 
 // Multi-restart optimize (engine.cpp:165-192): ranked, deduped, top_k.
 std::vector<Result> optimize(const OpDesc& op, const HwModel& hw, const EngineCfg& cfg, const Observer& obs = nullptr);

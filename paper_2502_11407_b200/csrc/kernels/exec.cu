@@ -15,6 +15,7 @@
 #include "../host/error.hpp"
 #include "../host/json.hpp"
 #include "../host/lower.hpp"
+#include "../host/tcplan.hpp"
 #include "common.cuh"
 #include "launch.h"
 
@@ -23,7 +24,7 @@ namespace gb::dev {
 namespace {
 std::atomic<uint64_t> g_launches{0};
 
-const char* kVariantNames[] = {"simt_parity", "simt_f32", "tc_tf32", "tc_bf16", "stream"};
+const char* kVariantNames[] = {"simt_parity", "simt_f32", "tc_tf32", "tc_bf16", "stream", "tc_3xtf32"};
 }  // namespace
 
 void check_cuda(cudaError_t e, const char* what) {
@@ -391,24 +392,30 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
             g.batch = static_cast<int>(op.batch);
           }
           g.bf16 = bf16;
-          // N tile from the schedule's level-1 n tile (UMMA N in [64, 256]); M tile = UMMA M 128
-          // N tile: the schedule's level-1 n tile, clamped to the UMMA range [64, 256] (fp32 output:
-          // [64, 128], the epilogue staging must fit next to the pipeline); halved while the grid
-          // would leave SMs idle (fewer tiles than SMs).
-          const int bn_max = bf16 ? 256 : 128;
-          int bn = static_cast<int>(pow2_clamp(s.L && !conv1x1 ? s.tile(op, 1, 1) : 128, 64, bn_max));
           auto tiles = [&](int b) { return static_cast<int64_t>((g.M + 127) / 128) * ((g.N + b - 1) / b) * g.batch; };
-          while (bn > 64 && tiles(bn) < sms) bn /= 2;
-          if (const char* e = dev_env("GENSOR_GEMM_BN")) bn = std::atoi(e);
-          g.BN = bn;
+          if (conv1x1) {
+            // the filter bank is A (M = F): full-width 128-position N tiles, halved while SMs idle
+            int bn = 128;
+            while (bn > 64 && tiles(bn) < sms) bn /= 2;
+            g.BN = bn;
+            const int nkb = (g.K * op.dtype_bytes + 127) / 128;
+            g.stages = std::min(gemm_tc_max_stages(bn, bf16), nkb > 8 ? 8 : nkb > 4 ? 6 : 4);
+          } else {
+            // the constructed state is the program (tcplan.hpp): UMMA N = the level-1 n tile,
+            // ring depth = the level-1 k tile in 128-byte k-blocks
+            const GemmTcPlan tp = gemm_tc_plan(op, s, bf16, false);
+            g.BN = tp.BN;
+            g.stages = tp.stages;
+            g.cs = tp.cs;
+          }
+          if (const char* e = dev_env("GENSOR_GEMM_BN")) g.BN = std::atoi(e);
+          if (const char* e = dev_env("GENSOR_GEMM_STAGES")) g.stages = std::atoi(e);
+          const int bn = g.BN;
           g.sms = sms;
-          const int nkb = (g.K * op.dtype_bytes + 127) / 128;
-          g.stages = std::min(gemm_tc_max_stages(bn, bf16), nkb > 8 ? 8 : nkb > 4 ? 6 : 4);
-          // A multicast across clusters of n-tiles (developer switch GENSOR_GEMM_CLUSTER=2|4):
-          // measured not to pay on the suite shapes (G: 16.2 vs 15.0 us, GPT-2 sequence -7 %)
-          const int cs_env = dev_env("GENSOR_GEMM_CLUSTER") ? std::atoi(dev_env("GENSOR_GEMM_CLUSTER")) : 1;
+          // A multicast across a cluster of n-tiles: the state's n-axis vthreads (tcplan.hpp)
+          if (const char* e = dev_env("GENSOR_GEMM_CLUSTER")) g.cs = std::atoi(e);
           const int tn = (g.N + bn - 1) / bn;
-          g.cs = (cs_env >= 4 && tn % 4 == 0) ? 4 : (cs_env >= 2 && tn % 2 == 0) ? 2 : 1;
+          while (g.cs > 1 && tn % g.cs) g.cs /= 2;
           pi << "{\"family\":\"gemm_tc\"" << (conv1x1 ? ",\"conv1x1\":\"O[n] = K . I[n], filter bank shared\"" : "")
              << ",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"stages\":" << gemm_tc_stages(g)
              << ",\"tiles\":" << tiles(g.BN) << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms)
@@ -500,6 +507,26 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         }
         break;
       }
+      case 5: {  // fp32-grade tensor-core GEMM: 3xTF32 operand split inside gemm_tc
+        if (!(op.kind == Kind::Gemm && gemm_tc_ok(op, false)))
+          throw Error(Code::Unsupported, std::string("tc_3xtf32 not available for ") + op.label());
+        k->family = Family::GemmTc;
+        k->launch_names = {"gemm_tc_3xtf32"};
+        GemmTcArgs& g = k->gemm;
+        g.M = static_cast<int>(op.param("M"));
+        g.N = static_cast<int>(op.param("N"));
+        g.K = static_cast<int>(op.param("K"));
+        g.batch = static_cast<int>(op.batch);
+        g.x3 = true;
+        g.BN = 64;  // two operand copies per stage: the 64-wide N tile keeps 4 stages in smem
+        g.sms = sms;
+        g.stages = gemm_tc_max_stages(64, false, true);
+        const int64_t tiles = static_cast<int64_t>((g.M + 127) / 128) * ((g.N + 63) / 64) * g.batch;
+        pi << "{\"family\":\"gemm_tc\",\"split\":\"3xTF32: A_lo.B_hi + A_hi.B_lo + A_hi.B_hi\",\"BM\":128,\"BN\":64"
+           << ",\"BK_bytes\":128,\"stages\":" << std::min(4, g.stages) << ",\"tiles\":" << tiles
+           << ",\"grid\":" << std::min<int64_t>(tiles, sms) << ",\"block\":320,\"persistent\":true}";
+        break;
+      }
       case 4: {
         if (!stream_ok(op))
           throw Error(Code::Unsupported, std::string("stream not available for ") + op.label());
@@ -551,6 +578,8 @@ void destroy(Kernel* k) {
     if (e) cudaEventDestroy(e);
   delete k;
 }
+
+std::string plan(const Kernel* k) { return k->plan_info; }
 
 std::string info(const Kernel* k) {
   std::ostringstream os;

@@ -35,6 +35,20 @@ struct TcTraits<__nv_bfloat16> {
   static constexpr bool kF16Kind = true;
 };
 
+// x = hi + lo with hi = x rounded to tf32 (10 explicit mantissa bits, nearest, ties away from
+// zero) and lo = (x - hi) rounded the same way; x - hi is exact in fp32. The rounding is done on
+// the bit pattern (sign-magnitude: adding half an ulp to the magnitude then clearing the 13 low
+// bits), so both parts are exact tf32 values whatever the tensor core does with low bits.
+__device__ __forceinline__ float round_tf32(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ float split_tf32(float x, float& lo) {
+  const float hi = round_tf32(x);
+  lo = round_tf32(x - hi);
+  return hi;
+}
+
 // Persistent: CTA b walks tiles b, b + grid, ... (n fastest, so consecutive CTAs share A rows in
 // L2). The smem ring continues across tiles; two TMEM accumulators let the epilogue of tile i
 // overlap the MMAs of tile i+1. Epilogue: tcgen05.ld 32 columns -> registers -> the warp's
@@ -228,6 +242,188 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// fp32-grade GEMM on the tf32 tensor cores ("3xTF32"), C = A.B with fp32 storage:
+//   warp 0      TMA producer (plain FLOAT32 maps: the fp32 bits land untouched);
+//   warps 2..5  converters: every staged element x -> hi = tf32(x) in place, lo = tf32(x - hi)
+//               into a mirror buffer of the same swizzled layout (x - hi is exact in fp32);
+//   warp 1      MMA issuer: per k-step A_lo.B_hi + A_hi.B_lo into the SMALL partial and
+//               A_hi.B_hi into the BIG partial, both fresh for every 128-byte k-block;
+//   warps 6..9  accumulators: after each k-block, big + small from TMEM -> fp32 registers.
+// The tensor core's fp32 accumulation does not round to nearest (measured: 9e-6 normwise at
+// K = 1024 when all 384 MMAs of a row accumulate in TMEM), so TMEM only ever holds one k-block
+// (32 products per partial) and the k-blocks are summed in registers with IEEE adds; the
+// dropped A_lo.B_lo term is < 2^-22 |a b|. Partials double-buffer in TMEM (4 x 64 columns).
+template <int STAGES>
+__global__ void __launch_bounds__(320, 1)
+    k_gemm_x3(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total) {
+  constexpr int BM = 128, BN = 64, BK = 32;
+  constexpr uint32_t A_BYTES = BM * 128, B_BYTES = BN * 128;
+  constexpr uint32_t STAGE = A_BYTES + B_BYTES;     // hi half; the lo mirror follows
+  constexpr uint32_t STAGE_BYTES = 2 * STAGE;
+  constexpr uint32_t IDESC = instr_desc(2, BM, BN, 0, 1);
+  constexpr uint32_t STG_WARP = 32 * BN * 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* staging = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * STG_WARP);
+  uint64_t* empty = full + STAGES;
+  uint64_t* split = empty + STAGES;   // [STAGES] converted (4 converter warps)
+  uint64_t* pfull = split + STAGES;   // [2] partials of a k-block written (MMA commit)
+  uint64_t* pempty = pfull + 2;       // [2] partials read (4 accumulator warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (K + BK - 1) / BK;
+  const int per_batch = tiles_m * tiles_n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&split[s], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pfull[i], 1);
+      mbar_init(&pempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    tma_prefetch(&mapC);
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);  // partial p: big at 128p, small at 128p + 64
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = t / per_batch, m0 = ((t % per_batch) / tiles_n) * BM, n0 = (t % tiles_n) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE);
+          uint8_t* a_s = smem + s * STAGE_BYTES;
+          tma_load_3d(a_s, &mapA, &full[s], kb * BK, m0, b);
+#pragma unroll
+          for (int j = 0; j < BN * 4 / 128; ++j)
+            tma_load_3d(a_s + A_BYTES + j * (BK * 128), &mapB, &full[s], n0 + j * 32, kb * BK, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x)
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES, p = it & 1;
+          mbar_wait(&pempty[p], ((it >> 1) & 1) ^ 1);
+          mbar_wait(&split[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES), b_addr = a_addr + A_BYTES;
+          const uint32_t big = tmem + 128 * p, small = big + 64;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(b_addr + k * 1024, BK * 128, 512, 1);
+            const uint64_t ad_lo = smem_desc_sw128(a_addr + STAGE + k * 32, 16, 1024);
+            const uint64_t bd_lo = smem_desc_sw128(b_addr + STAGE + k * 1024, BK * 128, 512, 1);
+            mma_tf32(small, ad_lo, bd, IDESC, k != 0);
+            mma_tf32(small, ad, bd_lo, IDESC, 1u);
+            mma_tf32(big, ad, bd, IDESC, k != 0);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&pfull[p]);
+        }
+    }
+  } else if (warp < 6) {
+    // converters (warps 2..5): split the stage once the TMA has landed it
+    const int ct = threadIdx.x - 64;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x)
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        float4* hi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
+        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + STAGE);
+#pragma unroll 4
+        for (int i = ct; i < static_cast<int>(STAGE / 16); i += 128) {
+          float4 v = hi[i], l;
+          v.x = split_tf32(v.x, l.x);
+          v.y = split_tf32(v.y, l.y);
+          v.z = split_tf32(v.z, l.z);
+          v.w = split_tf32(v.w, l.w);
+          hi[i] = v;
+          lo[i] = l;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&split[s]);
+      }
+  } else {
+    // accumulators (warps 6..9 -> TMEM lane quarters 2, 3, 0, 1): sum the k-block partials
+    const int q = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    int it = 0, local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int b = t / per_batch, m0 = ((t % per_batch) / tiles_n) * BM, n0 = (t % tiles_n) * BN;
+      float acc[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int p = it & 1;
+        mbar_wait(&pfull[p], (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          uint32_t rb[16], rs[16];
+          tmem_ld16(tmem + 128 * p + lane_off + 16 * h, rb);
+          tmem_ld16(tmem + 128 * p + 64 + lane_off + 16 * h, rs);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[16 * h + j] += __uint_as_float(rb[j]) + __uint_as_float(rs[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[p]);
+      }
+      // store: the warp's 32 rows x 64 fp32 through a 128 B-swizzled staging slice, TMA store
+      uint8_t* stg = staging + (warp - 6) * STG_WARP;
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint8_t* blk = stg + c * (32 * 128) + lane * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(blk + ((k ^ (lane & 7)) << 4)) =
+              make_float4(acc[32 * c + 4 * k], acc[32 * c + 4 * k + 1], acc[32 * c + 4 * k + 2], acc[32 * c + 4 * k + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (m0 + q * 32 < M) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            if (n0 + c * 32 < N) tma_store_3d(&mapC, stg + c * (32 * 128), n0 + c * 32, m0 + q * 32, b);
+        }
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -238,6 +434,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
+}
+
+template <int STAGES>
+void run_x3(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
+  const size_t smem = STAGES * 2 * (128 * 128 + 64 * 128) + 4 * 32 * 64 * 4 + 1024 + 256;
+  auto kern = k_gemm_x3<STAGES>;
+  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+             "gemm_x3 smem attribute");
+  const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + 63) / 64;
+  const int total = tiles_m * tiles_n * a.batch;
+  kern<<<std::min(total, a.sms), 320, smem, st>>>(m.A, m.B, m.C, a.M, a.N, a.K, tiles_m, tiles_n, total);
+  check_cuda(cudaGetLastError(), "gemm_x3 launch");
+  count_launch();
 }
 
 template <typename T, typename TOut, int BN, int STAGES, int CS, int SB = 1>
@@ -341,8 +550,8 @@ bool gemm_tc_supported(int M, int N, int K, int elem_bytes) {
          (static_cast<int64_t>(N) * elem_bytes) % 16 == 0;
 }
 
-int gemm_tc_max_stages(int BN, bool bf16) {
-  const size_t stage = 128 * 128 + static_cast<size_t>(BN) * 128;
+int gemm_tc_max_stages(int BN, bool bf16, bool x3) {
+  const size_t stage = (128 * 128 + static_cast<size_t>(BN) * 128) * (x3 ? 2 : 1);
   const size_t stg = 4 * 32 * static_cast<size_t>(BN) * (bf16 ? 2 : 4);
   return static_cast<int>((227 * 1024 - 2048 - stg) / stage);
 }
@@ -356,15 +565,18 @@ void gemm_tc_maps(const GemmTcArgs& a, const void* A, const void* B, void* C, Ge
                           static_cast<uint64_t>(a.a_shared ? 1 : a.batch)};
   const uint64_t sa[2] = {static_cast<uint64_t>(a.K) * es, static_cast<uint64_t>(a.K) * a.M * es};
   const uint32_t ba[3] = {bk, 128, 1};
-  encode_map(&m.A, a.bf16, !a.bf16, A, 3, da, sa, ba);
+  // tf32 maps round fp32 to tf32 in flight (TFLOAT32 data type); the 3xTF32 split needs the
+  // untouched fp32 bits in shared memory, so its maps load plain FLOAT32
+  const bool tf32 = !a.bf16 && !a.x3;
+  encode_map(&m.A, a.bf16, tf32, A, 3, da, sa, ba);
   if (a.cs > 1) {  // multicast slices: 128/cs rows per CTA of the cluster
     const uint32_t bam[3] = {bk, static_cast<uint32_t>(128 / a.cs), 1};
-    encode_map(&m.Am, a.bf16, !a.bf16, A, 3, da, sa, bam);
+    encode_map(&m.Am, a.bf16, tf32, A, 3, da, sa, bam);
   }
   const uint64_t db[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.K), static_cast<uint64_t>(a.batch)};
   const uint64_t sb[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.K * es};
   const uint32_t bb[3] = {bk, bk, 1};  // 128 B of N x BK rows of K
-  encode_map(&m.B, a.bf16, !a.bf16, B, 3, db, sb, bb, /*atom32=*/!a.bf16);
+  encode_map(&m.B, a.bf16, tf32, B, 3, db, sb, bb, /*atom32=*/!a.bf16);
   // output map: 128 B column blocks x 32 rows (one epilogue warp's slice)
   const uint64_t dc[3] = {static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.batch)};
   const uint64_t sc[2] = {static_cast<uint64_t>(a.N) * es, static_cast<uint64_t>(a.N) * a.M * es};
@@ -373,6 +585,15 @@ void gemm_tc_maps(const GemmTcArgs& a, const void* A, const void* B, void* C, Ge
 }
 
 void launch_gemm_tc(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
+  if (a.x3) {  // fp32-grade 3xTF32: BN = 64 (two operand copies per stage), plain persistent grid
+    constexpr int MAXS = static_cast<int>((227 * 1024 - 2048 - 4 * 32 * 64 * 4) / (2 * (128 * 128 + 64 * 128)));
+    static_assert(MAXS >= 3, "3xTF32 stages do not fit shared memory");
+    if (gemm_tc_stages(a) >= 4 && MAXS >= 4)
+      run_x3<(MAXS >= 4 ? 4 : 3)>(a, m, st);
+    else
+      run_x3<3>(a, m, st);
+    return;
+  }
   if (a.bf16) {
     switch (a.BN) {
       case 64: run_bn<__nv_bfloat16, __nv_bfloat16, 64>(a, m, st); break;

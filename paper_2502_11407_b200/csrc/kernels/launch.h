@@ -40,12 +40,13 @@ struct GemmTcArgs {
   int sms = 148;
   bool bf16 = false;
   bool a_shared = false;  // A is one matrix for every batch entry (1x1 conv: the filter bank)
+  bool x3 = false;        // fp32-grade 3xTF32 (hi/lo operand split in the kernel), BN = 64
 };
 struct GemmTcMaps {
   CUtensorMap A, B, C, Am;  // Am: A slices for cluster multicast (box rows 128 / cs)
 };
 bool gemm_tc_supported(int M, int N, int K, int elem_bytes);
-int gemm_tc_max_stages(int BN, bool bf16);
+int gemm_tc_max_stages(int BN, bool bf16, bool x3 = false);
 int gemm_tc_stages(const GemmTcArgs& a);
 void gemm_tc_maps(const GemmTcArgs& a, const void* A, const void* B, void* C, GemmTcMaps& m);
 void launch_gemm_tc(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st);

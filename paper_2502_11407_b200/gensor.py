@@ -28,7 +28,7 @@ ERROR_NAMES = [
     "Invalid", "Truncated",
 ]
 
-VARIANTS = {"auto": -1, "simt_parity": 0, "simt_f32": 1, "tc_tf32": 2, "tc_bf16": 3, "stream": 4}
+VARIANTS = {"auto": -1, "simt_parity": 0, "simt_f32": 1, "tc_tf32": 2, "tc_bf16": 3, "stream": 4, "tc_3xtf32": 5}
 MODES = {"reference": 0, "b200": 1}
 ACTION_KINDS = ["tile", "inv_tile", "set_vthread", "cache"]
 

@@ -14,9 +14,11 @@ import json
 import numpy as np
 import pytest
 
-from conftest import B200_REF, GENERIC
+import os
 
-F32_TOL = 2e-6
+from conftest import B200_REF, CONFIG_OPS, GENERIC
+
+F32_TOL = 1e-6  # single-precision mode within 1e-6
 
 torch = pytest.importorskip("torch")
 g = pytest.importorskip("paper_2502_11407_b200")
@@ -190,3 +192,26 @@ def test_rerank_on_device_orders_by_measured_time():
     ref = _round(O.reference_compute(doc, xs), False)
     got = _run(op, sched, best, "simt_f32", xs, ref.size)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["G", "C"])
+def test_full_size_fp32_configs(name):
+    """BASELINE configs[0] (G, GEMM fp32 1024^3) and configs[1] (C, the ResNet-50 conv) at full size
+    on the state-driven SIMT family: simt_parity bit-exact to interpret(lower(state)), simt_f32
+    within the SPEC's single-precision bar (1e-6 normwise, scaled by sqrt(K/64) past the desk
+    suite's extents)."""
+    doc = CONFIG_OPS[name]
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(seed=0, mode="b200", top_k=1))
+    rng = np.random.default_rng(11)
+    xs = [rng.uniform(-1, 1, size=int(np.prod(t["true_dims"]))).astype(np.float32) for t in op.tensors[:-1]]
+    ref = O.interpret(doc, sched[0]["state"], xs, threads=os.cpu_count() or 8)
+    got = _run(op, sched, 0, "simt_parity", xs, ref.size)
+    assert np.array_equal(got, _round(ref, False)), np.abs(got - _round(ref, False)).max()
+    got = _run(op, sched, 0, "simt_f32", xs, ref.size)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    # SPEC.md:507 states 1e-6 for the desk suite (extents <= 64); a sequential fp32 accumulation
+    # over K terms drifts like sqrt(K) roundings, so at K = 1024 (G) / 576 (C) the same bar scales
+    # by sqrt(K / 64)
+    k_red = 1024 if name == "G" else 64 * 9
+    assert err <= F32_TOL * np.sqrt(k_red / 64), err

@@ -17,8 +17,8 @@ import pytest
 
 from conftest import B200_REF, GENERIC
 
-STREAM_TOL = 2e-6
-SOFTMAX_RTOL = 2e-6
+STREAM_TOL = 1e-6  # SPEC.md:563 single-precision bar, normwise
+SOFTMAX_RTOL = 1e-6
 
 torch = pytest.importorskip("torch")
 g = pytest.importorskip("paper_2502_11407_b200")
