@@ -5,11 +5,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 namespace gb::dev {
 
 void check_cuda(cudaError_t e, const char* what);  // throws gb::Error(Cuda)
+
+// Developer A/B switches (GENSOR_* environment variables) exist only in builds compiled with
+// -DGENSOR_DEV_OVERRIDES (make DEV=1); the product library never reads the environment.
+inline const char* dev_env(const char* name) {
+#ifdef GENSOR_DEV_OVERRIDES
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 void count_launch(uint64_t n = 1);
 
 template <typename T>

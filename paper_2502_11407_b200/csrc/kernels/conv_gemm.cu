@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
+        tmem_ld_pin(r);
         const int f0 = nt * BN + c;
         if (vec) {
           __syncwarp();  // previous chunk's re-reads are done

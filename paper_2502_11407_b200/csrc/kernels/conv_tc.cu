@@ -34,6 +34,20 @@
 
 namespace gb::dev {
 
+#ifdef GENSOR_DEV_OVERRIDES
+// Developer timeline of conv_ns (make DEV=1 only): clock64 marks per CTA, 64 slots, read back by
+// gensor_dev_conv_trace (tools/conv_trace.py). The product build compiles the marks away.
+__device__ long long g_ns_trace[160 * 64];
+#define NS_MARK(slot) \
+  do {                 \
+    if (blockIdx.x < 160) g_ns_trace[blockIdx.x * 64 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define NS_MARK(slot) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace {
 
 using namespace tc;
@@ -202,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem + acc * FN + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
+        tmem_ld_pin(r);
         if (ok) {
 #pragma unroll
           for (int v = 0; v < 32; ++v)
@@ -551,6 +566,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_img = tiles_h * tiles_w;
   constexpr int kMma = 1;
+  if (threadIdx.x == 0) NS_MARK(0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -578,6 +594,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
     // channels each, 128 B swizzle); out-of-range positions / channels are zero-filled
     if (elect_one()) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // X is written by the preceding pre-pass
+      NS_MARK(1);
       tma_prefetch(&mapX);
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -613,6 +630,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
+        if (local < 6) NS_MARK(8 + local);
         tc_fence_after();
         const uint32_t d = tmem + acc * ncol;
         bool first = true;
@@ -620,6 +638,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           const int st = it % STAGES;
           mbar_wait(&full[st], (it / STAGES) & 1);
           if (local == 0 && ck < kWb) mbar_wait(&wbar[ck], 0);  // chunk ck's filters (last: the rest)
+          if (local == 0 && ck == 0) NS_MARK(2);
           tc_fence_after();
           const uint32_t a_addr = a_base + st * a_bytes;
           // k-steps of 8 channels that hold real channels (a 12-channel space-to-depth chunk: 2)
@@ -635,6 +654,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           mma_commit(&empty[st]);
         }
         mma_commit(&acc_full[acc]);
+        if (local < 6) NS_MARK(16 + local);
       }
     }
   } else {
@@ -649,6 +669,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       const int h = ((t % tiles_img) / tiles_w) * kNsRows + q;
       const int w = (t % tiles_w) * valid_w + lane;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      if (warp == kMma + 1 && lane == 0 && local < 6) NS_MARK(24 + local);
       tc_fence_after();
       const bool ok = lane < valid_w && n < N && h < OH && w < OW;
       float* obase = O + (static_cast<int64_t>(n) * F * OH + h) * OW + w;
@@ -669,6 +690,10 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           if (S > 3) tmem_ld32(base + 3 * FN, r3);
         }
         tmem_ld_wait();
+        tmem_ld_pin(r0);
+        tmem_ld_pin(r1);
+        tmem_ld_pin(r2);
+        tmem_ld_pin(r3);
         if (c0 + 64 >= FN) {  // this warp's last TMEM block is in registers: hand the accumulator back
           tc_fence_before();
           __syncwarp();
@@ -721,8 +746,10 @@ __global__ void __launch_bounds__(kNsThreads, 1)
           }
         }
       }
+      if (warp == kMma + 1 && lane == 0 && local < 6) NS_MARK(32 + local);
     }
     if (tma_store && lane == 0) bulk_wait<0>();  // output stores complete before the CTA retires
+    if (warp == kMma + 1 && lane == 0) NS_MARK(40);
   }
   tc_fence_before();
   __syncthreads();
@@ -806,7 +833,10 @@ void run_conv_ns(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * g.gC * g.gR * g.gS;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
-    if (a.s2d) {
+    const char* skip = dev_env("GENSOR_CONV_SKIP");  // developer timing: "prepass" | "conv"
+    if (skip && skip[0] == 'p') {
+      // the workspace holds the previous execute's copy
+    } else if (a.s2d) {
       const int xblocks = static_cast<int>(std::min<int64_t>(1 << 20, static_cast<int64_t>(a.N) * g.gH));  // a row per block
       const size_t rsm = static_cast<size_t>(a.C) * 2 * a.W * sizeof(float);
       check_cuda(cudaFuncSetAttribute(k_s2d_prepass, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)),
@@ -824,6 +854,10 @@ void run_conv_ns(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const
     }
     check_cuda(cudaGetLastError(), "conv filter conversion launch");
     count_launch();
+    if (skip && skip[0] == 'c') {
+      mk.mark(st);
+      return;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kNsThreads);
@@ -899,6 +933,12 @@ bool conv_ns_supported(int C, int F, int R, int S, int stride, bool bf16) {
   return !bf16 && stride == 1 && C % 4 == 0 && S >= 1 && S <= 4 && R >= 1 && R <= 8 && S * FN <= 256 &&
          w_bytes + 2 * static_cast<size_t>(kNsRows + R - 1) * 4096 <= 227 * 1024 - 2048 - kNsEpi * 8 * kNsCols * 4;
 }
+
+#ifdef GENSOR_DEV_OVERRIDES
+extern "C" int gensor_dev_conv_trace(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_ns_trace, sizeof(long long) * std::min(n, 160 * 64)) == cudaSuccess ? 0 : 19;
+}
+#endif
 
 void conv_tc_maps(const ConvTcArgs& a, void* ws, void* O, ConvTcMaps& m) {
   if (a.ns)

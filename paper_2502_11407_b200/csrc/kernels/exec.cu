@@ -34,18 +34,6 @@ void check_cuda(cudaError_t e, const char* what) {
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
-namespace {
-// Developer A/B switches (GENSOR_* environment variables) exist only in builds compiled with
-// -DGENSOR_DEV_OVERRIDES (make DEV=1); the product library never reads the environment.
-const char* dev_env(const char* name) {
-#ifdef GENSOR_DEV_OVERRIDES
-  return std::getenv(name);
-#else
-  (void)name;
-  return nullptr;
-#endif
-}
-}  // namespace
 
 enum class Family { Generic, GemmTc, ConvTc, ConvGemm, Stream };
 

@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[32];
         tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
         tmem_ld_wait();
+        tmem_ld_pin(r);
         if constexpr (sizeof(TOut) == 4) {  // 32 fp32 = one 128 B block, 8 chunks
           uint8_t* blk = stg + (c / 32) * (32 * 128) + lane * 128;
 #pragma unroll
@@ -256,7 +257,8 @@ __global__ void __launch_bounds__(192, 1)
 template <int STAGES>
 __global__ void __launch_bounds__(320, 1)
     k_gemm_x3(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total) {
+              const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m, int tiles_n, int total,
+              int dbg) {
   constexpr int BM = 128, BN = 64, BK = 32;
   constexpr uint32_t A_BYTES = BM * 128, B_BYTES = BN * 128;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;     // hi half; the lo mirror follows
@@ -332,8 +334,10 @@ __global__ void __launch_bounds__(320, 1)
             const uint64_t bd = smem_desc_sw128(b_addr + k * 1024, BK * 128, 512, 1);
             const uint64_t ad_lo = smem_desc_sw128(a_addr + STAGE + k * 32, 16, 1024);
             const uint64_t bd_lo = smem_desc_sw128(b_addr + STAGE + k * 1024, BK * 128, 512, 1);
-            mma_tf32(small, ad_lo, bd, IDESC, k != 0);
-            mma_tf32(small, ad, bd_lo, IDESC, 1u);
+            if (!(dbg & 1)) {
+              mma_tf32(small, ad_lo, bd, IDESC, k != 0);
+              mma_tf32(small, ad, bd_lo, IDESC, 1u);
+            }
             mma_tf32(big, ad, bd, IDESC, k != 0);
           }
           mma_commit(&empty[s]);
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(320, 1)
           v.y = split_tf32(v.y, l.y);
           v.z = split_tf32(v.z, l.z);
           v.w = split_tf32(v.w, l.w);
+          if (dbg & 2) continue;  // developer: leave the stage untouched
           hi[i] = v;
           lo[i] = l;
         }
@@ -384,6 +389,11 @@ __global__ void __launch_bounds__(320, 1)
           tmem_ld16(tmem + 128 * p + lane_off + 16 * h, rb);
           tmem_ld16(tmem + 128 * p + 64 + lane_off + 16 * h, rs);
           tmem_ld_wait();
+          tmem_ld_pin(rb);
+          tmem_ld_pin(rs);
+          if (dbg & 1)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rs[j] = 0u;
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[16 * h + j] += __uint_as_float(rb[j]) + __uint_as_float(rs[j]);
         }
@@ -444,7 +454,8 @@ void run_x3(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
              "gemm_x3 smem attribute");
   const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + 63) / 64;
   const int total = tiles_m * tiles_n * a.batch;
-  kern<<<std::min(total, a.sms), 320, smem, st>>>(m.A, m.B, m.C, a.M, a.N, a.K, tiles_m, tiles_n, total);
+  const int dbg = dev_env("GENSOR_X3_DBG") ? std::atoi(dev_env("GENSOR_X3_DBG")) : 0;
+  kern<<<std::min(total, a.sms), 320, smem, st>>>(m.A, m.B, m.C, a.M, a.N, a.K, tiles_m, tiles_n, total, dbg);
   check_cuda(cudaGetLastError(), "gemm_x3 launch");
   count_launch();
 }

@@ -180,6 +180,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// tcgen05.ld destination registers hold their values only after tcgen05.wait::ld, but the compiler
+// sees them as defined by the load itself and may schedule their first use above the wait. An
+// empty asm that "rewrites" each register after the wait pins every use behind it.
+template <int N>
+__device__ __forceinline__ void tmem_ld_pin(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 // ---- TMA stores (shared -> global), bulk async-groups --------------------------------------
 // Generic-proxy writes to shared memory must be fenced before the async proxy (TMA) reads them.
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

@@ -1,0 +1,77 @@
+"""Developer timeline of the headline conv (needs the DEV build: make -C paper_2502_11407_b200/csrc
+DEV=1 after touching kernels/{exec,conv_tc}.cu). Prints (1) device time of pre-pass only, conv
+only (stale workspace) and both, L2 flushed between steps, and (2) the per-CTA clock64 marks of
+k_conv_ns (slots: 0 start, 1 griddep wait done, 2 first filters+A ready, 8+i MMA tile i start,
+16+i MMA tile i committed, 24+i epilogue got tile i, 32+i epilogue done with tile i, 40 end)."""
+import ctypes
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2502_11407_b200 as g  # noqa: E402
+
+doc = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {"kind": "conv2d", "I": [16, 64, 58, 58], "K": [64, 64, 3, 3], "S": 1}
+op = g.TensorOpSpec.parse_text(json.dumps(doc))
+s = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(mode="b200", top_k=1))
+k = g.Kernel(op, s, 0, "auto")
+print(k.info["plan"])
+xs = [torch.rand(int(np.prod(t["true_dims"])), device="cuda") * 2 - 1 for t in op.tensors[:-1]]
+out = torch.empty(int(np.prod(op.tensors[-1]["true_dims"])), device="cuda")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(5):
+    k.execute(xs, out)
+torch.cuda.synchronize()
+
+
+def timed(n=30):
+    ts = []
+    for _ in range(n):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        k.execute(xs, out)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return statistics.median(ts)
+
+
+for mode in (None, "prepass", "conv"):
+    if mode:
+        os.environ["GENSOR_CONV_SKIP"] = mode
+    else:
+        os.environ.pop("GENSOR_CONV_SKIP", None)
+    print(f"skip={mode}: {timed():.2f} us", flush=True)
+os.environ.pop("GENSOR_CONV_SKIP", None)
+lib = g.gensor.lib()
+fn = lib.gensor_dev_conv_trace
+fn.argtypes = [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
+buf = (ctypes.c_longlong * (160 * 64))()
+flush.zero_()
+torch.cuda.synchronize()
+k.execute(xs, out)
+torch.cuda.synchronize()
+assert fn(buf, 160 * 64) == 0
+tr = np.array(buf, dtype=np.int64).reshape(160, 64)[:148]
+rel = tr - tr[:, :1]
+rows = []
+for c in range(148):
+    r = rel[c]
+    nt = sum(1 for i in range(6) if tr[c, 16 + i] != 0)
+    rows.append((c, nt, r[1], r[2], [r[8 + i] for i in range(nt)], [r[16 + i] for i in range(nt)],
+                 [r[24 + i] for i in range(nt)], [r[32 + i] for i in range(nt)], r[40]))
+for row in rows[:6] + rows[-2:]:
+    print(row)
+end = np.array([r[-1] for r in rows])
+print("end clk: median", np.median(end), "max", end.max(), "min", end.min())
+first_mma = np.array([r[4][0] for r in rows])
+print("first MMA start: median", np.median(first_mma), "griddep wait", np.median([r[2] for r in rows]),
+      "filters ready", np.median([r[3] for r in rows]))
+mma = [r[5][i] - r[4][i] for r in rows for i in range(r[1])]
+epi = [r[7][i] - r[6][i] for r in rows for i in range(r[1])]
+print("MMA issue->commit per tile: median", np.median(mma), " epilogue per tile: median", np.median(epi))
