@@ -821,12 +821,12 @@ def run_ours(args):
                            sp.get("variant", "auto"), flush, e2e=False)
                 ki = r["kernel"].info
                 w = r["flops"] if sp["unit"] == "TFLOP/s" else r["bytes"]
-                rl = roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname))
+                srl = roofline(r, sp, peaks, tf32, ki["variant_name"], ncu_traffic(wname))
                 suite[wname] = {
                     "variant": ki["variant_name"], "family": ki["plan"].get("family"),
                     "value": w / (statistics.mean(r["step_ms"]) / 1e3) / (1e12 if sp["unit"] == "TFLOP/s" else 1e9),
                     "unit": sp["unit"], "ms_per_step": statistics.mean(r["step_ms"]),
-                    "roofline": {k: rl[k] for k in ("bound", "achieved", "peak", "frac", "traffic", "kernel")},
+                    "roofline": {k: srl[k] for k in ("bound", "achieved", "peak", "frac", "traffic", "kernel")},
                     "construction_s": r["construct_s"],
                 }
                 del r
