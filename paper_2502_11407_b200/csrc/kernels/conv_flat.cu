@@ -1,0 +1,553 @@
+// conv_flat: stride-1 tf32 conv2d that reads the caller's NCHW input IN PLACE through TMA (no
+// NHWC copy of the activations).
+//
+// Flattened planes. With stride 1, output (h, w) of image n reads input position
+// p + r*W + s of every channel plane, where p = h*W + w is the output's position in the INPUT's
+// row pitch ("wide" positions; the W - OW columns past each output row are computed and
+// dropped). So every tap (r, s) is a 1-D shift o = r*W + s of one flat plane, and a tile of 128
+// consecutive wide positions is an M = 128 UMMA tile whose A operand (positions x channels) is
+// MN-major: 32 consecutive positions of one channel are one 128 B row, exactly what a TMA box
+// over the plane-major input {H*W, N*C} delivers (32 B-atom swizzle, the tf32 MN-major layout).
+//
+// Alignment. TMA can only start a box at a 16 B-aligned position (tools/tma_align_probe.cu), so a
+// tap is split as o = a + b with a = o & ~3 (the A box offset) and b = o & 3. The MMA for tap
+// (r, s) multiplies the box at P0 + a and lands in TMEM accumulator block b; the epilogue adds
+// block b of TMEM lane j + b into output j. Taps sharing an offset a share one staged A box and
+// are folded into the UMMA N (3x3 over a 58-wide plane: a = 0 {b 0,1,2 -> N 192}, 56 {b 2,3 ->
+// N 128}, 60 {b 0 -> N 64}, 116 {b 0,1,2 -> N 192}); their filter rows sit next to each other in
+// the resident bank. Lanes j + b >= 32 belong to the next warp's lane quarter: the first three
+// lanes of each warp publish their blocks 1..3 through shared memory. Tiles advance by 124
+// positions (multiple of 4, lanes 124..127 only feed their neighbours).
+//
+// Two launches, chained by programmatic dependent launch: k_flat_filters converts K[f][c][r][s]
+// into the bank image W' (K-major, 128 B-swizzled, tf32-rounded; one 147 KB copy per execute in
+// the workspace) while the conv grid starts and streams its first input stages; the conv CTAs
+// then copy W' into shared memory with one bulk copy per 32-channel chunk.
+//
+// Roles: warp 0 = TMA producer (one 16 KB stage per (tile, 32-channel chunk, offset group)),
+// warp 1 = MMA issuer (a precomputed op table: accumulator column, filter rows, UMMA N, first-touch
+// flag), warps 2.. = epilogue (EPW warps per TMEM lane quarter, splitting the 16-filter blocks).
+// Accumulators: 4 blocks of FN columns, double-buffered (2 x 256 TMEM columns), so tile i's
+// epilogue overlaps tile i+1's MMAs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <utility>
+#include <cstdlib>
+#include <string>
+
+#include "../host/error.hpp"
+#include "common.cuh"
+#include "launch.h"
+#include "tc_common.cuh"
+
+namespace gb::dev {
+using namespace tc;
+
+#ifdef GENSOR_DEV_OVERRIDES
+// Developer timeline (make DEV=1 only): clock64 marks per CTA, 64 slots (tools/conv_trace.py):
+// 0 start, 1 bank requested, 8+i MMA tile i start, 16+i tile i committed, 24+i epilogue got tile i,
+// 32+i epilogue done with tile i, 40 MMA loop end, 44/45 epilogue of tile 1: blocks read /
+// boundary values exchanged.
+__device__ long long g_flat_trace[160 * 64];
+#define FL_MARK(slot) \
+  do {                 \
+    if (blockIdx.x < 160) g_flat_trace[blockIdx.x * 64 + (slot)] = clock64(); \
+  } while (0)
+#define FL_CLOCK() clock64()
+#define FL_STORE(slot, v) \
+  do {                     \
+    if (blockIdx.x < 160) g_flat_trace[blockIdx.x * 64 + (slot)] = (v); \
+  } while (0)
+extern "C" int gensor_dev_flat_trace(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_flat_trace, sizeof(long long) * std::min(n, 160 * 64)) == cudaSuccess ? 0 : 19;
+}
+#else
+#define FL_MARK(slot) \
+  do {                 \
+  } while (0)
+#define FL_CLOCK() 0ll
+#define FL_STORE(slot, v) \
+  do {                     \
+  } while (0)
+#endif
+
+namespace {
+
+constexpr int kFlatStep = 124;     // tile advance (lanes 124..127 are only read by their neighbours)
+constexpr int kFlatStage = 16384;  // one A stage: 4 boxes of 32 positions x 32 channels x 4 B
+constexpr int kFlatXFloats = 96;   // per warp and 16-filter block: [b1 L0][b2 L0,L1][b3 L0,L1,L2]
+constexpr int kFlatMaxChunks = 8;  // bank barriers (one per 32-channel chunk, the last takes the rest)
+constexpr int kFlatEpw = 4;        // epilogue warps per TMEM lane quarter (one 16-filter block each at FN = 64)
+constexpr int kFlatNfbh = 1;       // 16-filter blocks per epilogue warp (FN <= 64)
+
+// round to tf32 (nearest, ties away — cvt.rna.tf32.f32) with two integer ops; Inf / NaN unchanged
+__device__ __forceinline__ uint32_t f32_to_tf32(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x7f800000u) == 0x7f800000u ? u : (u + 0x1000u) & 0xffffe000u;
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// ---- bank image W'[chunk][slot(t)][f][32 c] (K-major rows of 128 B, 128 B swizzle: 16 B granule
+// g of row rho stored at g ^ (rho & 7)), tf32-rounded, rows f >= F zero. One thread per (f, 4
+// channels, tap): four strided loads of K, one 16 B store.
+__global__ void __launch_bounds__(128) k_flat_filters(const float* __restrict__ K, uint8_t* __restrict__ Wp,
+                                                      const __grid_constant__ ConvFlatArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the conv grid may start now
+  const int c4n = a.C >> 2;
+  const int total = a.FN * c4n * a.T;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int t = e % a.T;
+  const int u = e / a.T;
+  const int f = u / c4n, c4 = u - f * c4n;
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (f < a.F) {
+    const float* src = K + (static_cast<int64_t>(f) * a.C + 4 * c4) * a.T + t;
+    v = make_uint4(f32_to_tf32(__ldg(src)), f32_to_tf32(__ldg(src + a.T)), f32_to_tf32(__ldg(src + 2 * a.T)),
+                   f32_to_tf32(__ldg(src + 3 * a.T)));
+  }
+  const int row = a.tb.tap_slot[t] * a.FN + f;
+  const size_t off = static_cast<size_t>(c4 >> 3) * a.T * a.FN * 128 + static_cast<size_t>(row) * 128 +
+                     ((((c4 & 7) ^ (row & 7))) << 4);
+  *reinterpret_cast<uint4*>(Wp + off) = v;
+}
+
+// ---- MMA issue: the table-driven loop (any shape) and the compile-time-specialised one (the op
+// table is a template constant: every descriptor offset, N and flag folds into the instruction
+// stream; tools/flat_rate.cu measured the table-driven issue at 3.7 k vs 2.6 k cycles per tile)
+struct FlatIssueCtx {
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* bank_bar;
+  uint64_t adesc0, bdesc_ck;
+  uint32_t d;
+  int it, local, ck;
+};
+
+template <int R, int S, int WM, int FN>
+struct FlatSpec {
+  static constexpr FlatTable t = flat_table(R, S, flat_rep_w(S, WM), FN);
+};
+
+template <class TB, int PASS, int G, int I>
+__device__ __forceinline__ void flat_op(const FlatIssueCtx& c, uint64_t ad) {
+  constexpr int o = TB::t.grp_op0[PASS][G] + I;
+  constexpr uint32_t idesc = instr_desc(2, 128, static_cast<uint32_t>(TB::t.op_n[o]), 1, 0);
+  constexpr uint32_t dcol = static_cast<uint32_t>(TB::t.op_dcol[o]);
+  constexpr uint64_t boff = static_cast<uint64_t>(TB::t.op_brow[o]) * 128 / 16;
+  constexpr uint32_t acc0 = TB::t.op_zero[o] ? 0u : 1u;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) mma_tf32(c.d + dcol, ad + kk * 64, c.bdesc_ck + boff + kk * 2, idesc, kk == 0 ? acc0 : 1u);
+}
+
+template <int STAGES, class TB, int PASS, int G, int... I>
+__device__ __forceinline__ void flat_stage(FlatIssueCtx& c, std::integer_sequence<int, I...>) {
+  const int st = c.it % STAGES;
+  mbar_wait(&c.full[st], (c.it / STAGES) & 1);
+  if (c.local == 0 && G == 0 && c.ck < kFlatMaxChunks) mbar_wait(&c.bank_bar[c.ck], 0);
+  tc_fence_after();
+  const uint64_t ad = c.adesc0 + static_cast<uint64_t>(st * (kFlatStage >> 4));
+  (flat_op<TB, PASS, G, I>(c, ad), ...);
+  mma_commit(&c.empty[st]);
+  ++c.it;
+}
+
+template <int STAGES, class TB, int PASS, int... G>
+__device__ __forceinline__ void flat_chunk(FlatIssueCtx& c, std::integer_sequence<int, G...>) {
+  (flat_stage<STAGES, TB, PASS, G>(c, std::make_integer_sequence<int, TB::t.grp_nop[PASS][G]>{}), ...);
+}
+
+template <int STAGES, class TB>
+__global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
+    k_conv_flat(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ ConvFlatArgs a,
+                const uint8_t* __restrict__ Wp, float* __restrict__ O) {
+  constexpr int EPW = kFlatEpw;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024 B-aligned base derived by pointer arithmetic (keeps the shared state space: LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int FN = a.FN, nck = a.nck;
+  const FlatTable& tb = a.tb;
+  const uint32_t blk = static_cast<uint32_t>(a.T * FN) * 128;  // one 32-channel chunk of the bank
+  uint8_t* bank = smem;
+  uint8_t* ring = smem + nck * blk;
+  const int nfb = FN / 16;
+  float* xbuf = reinterpret_cast<float*>(ring + STAGES * kFlatStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * kFlatNfbh * EPW * 4 * kFlatXFloats);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bank_bar = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bank_bar + kFlatMaxChunks);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) FL_MARK(0);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4 * min(EPW, nfb));  // epilogue warps that own a filter block
+    }
+    for (int i = 0; i < kFlatMaxChunks; ++i) mbar_init(&bank_bar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- producer: per (tile, chunk, offset group) one stage of 4 boxes {32 positions, 32 planes}
+    // (the input does not depend on the filter launch: no griddepcontrol.wait here)
+    if (elect_one()) {
+      tma_prefetch(&mapX);
+      int it = 0;
+      for (int t = blockIdx.x; t < a.total; t += gridDim.x) {
+        const int n = t / a.tiles_img;
+        const int p0 = (t - n * a.tiles_img) * kFlatStep;
+        for (int ck = 0; ck < nck; ++ck) {
+          const int plane = n * a.C + ck * 32;
+          for (int g = 0; g < tb.ngroups; ++g, ++it) {
+            const int st = it % STAGES;
+            mbar_wait_sleep(&empty[st], ((it / STAGES) & 1) ^ 1);
+            if ((a.exp & 4) && it >= STAGES) {  // DEV experiment: no TMA after the first ring (timing only)
+              mbar_arrive(&full[st]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&full[st], kFlatStage);
+            uint8_t* dst = ring + st * kFlatStage;
+            const int x0 = p0 + (tb.group_o[g] & ~3);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) tma_load_2d(dst + m * 4096, &mapX, &full[st], x0 + 32 * m, plane);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA issuer. The bank comes from the preceding filter launch: wait for it, then one bulk
+    // copy per 32-channel chunk (the first tile's MMAs on chunk 0 start before chunk 1 lands).
+    if (elect_one()) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int ck = 0; ck < nck; ++ck) {
+        uint64_t* bb = &bank_bar[ck < kFlatMaxChunks ? ck : kFlatMaxChunks - 1];
+        if (ck < kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blk);
+        else if (ck == kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blk * (nck - ck));
+        bulk_g2s(bank + ck * blk, Wp + static_cast<size_t>(ck) * blk, blk, bb);
+      }
+      FL_MARK(1);
+      FlatIssueCtx c;
+      c.full = full;
+      c.empty = empty;
+      c.bank_bar = bank_bar;
+      c.adesc0 = smem_desc_sw128(smem_u32(ring), 4096, 512, 1);
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(bank), 16, 1024);
+      c.it = 0;
+      c.local = 0;
+      for (int t = blockIdx.x; t < a.total; t += gridDim.x, ++c.local) {
+        const int acc = c.local & 1;
+        mbar_wait(&acc_empty[acc], ((c.local >> 1) & 1) ^ 1);
+        if (c.local < 6) FL_MARK(8 + c.local);
+        tc_fence_after();
+        c.d = tmem + acc * 256;
+        for (c.ck = 0; c.ck < nck; ++c.ck) {
+          c.bdesc_ck = bdesc0 + ((static_cast<uint64_t>(c.ck) * blk) >> 4);
+          if constexpr (!std::is_same_v<TB, void>) {
+            if (c.ck == 0)
+              flat_chunk<STAGES, TB, 0>(c, std::make_integer_sequence<int, TB::t.ngroups>{});
+            else
+              flat_chunk<STAGES, TB, 1>(c, std::make_integer_sequence<int, TB::t.ngroups>{});
+          } else {
+            const int pass = c.ck == 0 ? 0 : 1;
+            for (int g = 0; g < tb.ngroups; ++g) {
+              const int st = c.it % STAGES;
+              mbar_wait(&full[st], (c.it / STAGES) & 1);
+              if (c.local == 0 && g == 0 && c.ck < kFlatMaxChunks) mbar_wait(&bank_bar[c.ck], 0);
+              tc_fence_after();
+              const uint64_t ad = c.adesc0 + static_cast<uint64_t>(st * (kFlatStage >> 4));
+              const int o0 = tb.grp_op0[pass][g], o1 = o0 + tb.grp_nop[pass][g];
+              for (int o = o0; o < o1; ++o) {
+                const uint32_t dc = c.d + tb.op_dcol[o];
+                const uint64_t bd = c.bdesc_ck + static_cast<uint64_t>(tb.op_brow[o]) * 8;  // rows * 128 B >> 4
+                const uint32_t idesc = instr_desc(2, 128, static_cast<uint32_t>(tb.op_n[o]), 1, 0);
+                const uint32_t acc0 = tb.op_zero[o] ? 0u : 1u;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) mma_tf32(dc, ad + kk * 64, bd + kk * 2, idesc, kk == 0 ? acc0 : 1u);
+              }
+              mma_commit(&empty[st]);
+              ++c.it;
+            }
+          }
+        }
+        mma_commit(&acc_full[acc]);
+        if (c.local < 6) FL_MARK(16 + c.local);
+      }
+      FL_MARK(40);
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: warp w owns TMEM lane quarter q = w % 4 (tile rows 32q..32q+31) and the
+    // 16-filter blocks fb = h, h + EPW (at most kFlatNfbh); out(j) = sum_b D[lane j + b][block b].
+    // All of a warp's blocks are read first (the accumulator is released right away), published,
+    // one barrier per tile, then summed and stored.
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int nmine = h < nfb ? (nfb - h + EPW - 1) / EPW : 0;  // this warp's 16-filter blocks
+    const int nloop = nmine ? a.total : 0;
+    const int plane_out = a.OH * a.OW;
+    const uint32_t bm = tb.bmask;
+    int local = 0;
+    for (int t = blockIdx.x; t < nloop; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int n = t / a.tiles_img;
+      const int p0 = (t - n * a.tiles_img) * kFlatStep;
+      const int vt = min(kFlatStep, a.PW - p0);
+      const int j = q * 32 + lane;
+      const int p = p0 + j;
+      const int hrow = p / a.W, wcol = p - hrow * a.W;
+      const bool ok = j < vt && wcol < a.OW;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      if (warp == 2 && lane == 0 && local < 6) FL_MARK(24 + local);
+      tc_fence_after();
+      if (a.exp & 32) {  // DEV experiment: epilogue does nothing but release (timing only)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        continue;
+      }
+      uint32_t r[kFlatNfbh][4][16];
+#pragma unroll
+      for (int x = 0; x < kFlatNfbh; ++x) {
+        if (x < nmine) {
+          const uint32_t base =
+              tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>((h + x * EPW) * 16);
+          if (bm & 1u) tmem_ld16(base, r[x][0]);
+          if (bm & 2u) tmem_ld16(base + FN, r[x][1]);
+          if (bm & 4u) tmem_ld16(base + 2 * FN, r[x][2]);
+          if (bm & 8u) tmem_ld16(base + 3 * FN, r[x][3]);
+        }
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int x = 0; x < kFlatNfbh; ++x)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) tmem_ld_pin(r[x][b]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);  // the accumulator may take tile t + 2 now
+      if (warp == 2 && lane == 0 && local == 1) FL_MARK(44);
+      if (bm != 15u) {  // blocks no tap lands in are zero (the sums below need no per-block test)
+#pragma unroll
+        for (int x = 0; x < kFlatNfbh; ++x)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (!(bm & 1u)) r[x][0][i] = 0u;
+            if (!(bm & 2u)) r[x][1][i] = 0u;
+            if (!(bm & 4u)) r[x][2][i] = 0u;
+            if (!(bm & 8u)) r[x][3][i] = 0u;
+          }
+      }
+      // lanes L < 3 publish their blocks b > L (the previous quarter's lanes 32 - b + L need
+      // them), then take the NEXT quarter's lane-L values of those blocks into the same registers:
+      // after that, block b of output lane l is lane (l + b) & 31 of this warp (records parity-
+      // double-buffered; quarter 3's lanes 29..31 are rows >= 125, never stored)
+      auto put16 = [&](float* dst, const uint32_t(&v)[16]) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          reinterpret_cast<uint4*>(dst)[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+      };
+      auto get16 = [&](const float* src, uint32_t(&v)[16]) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint4 y = reinterpret_cast<const uint4*>(src)[k];
+          v[4 * k] = y.x, v[4 * k + 1] = y.y, v[4 * k + 2] = y.z, v[4 * k + 3] = y.w;
+        }
+      };
+      float* rec = xbuf + (((local & 1) * EPW + h) * 4) * (kFlatNfbh * kFlatXFloats);
+      if (lane < 3) {
+#pragma unroll
+        for (int x = 0; x < kFlatNfbh; ++x) {
+          float* mine = rec + (q * kFlatNfbh + x) * kFlatXFloats;
+          if (lane == 0) put16(mine, r[x][1]);
+          if (lane < 2) put16(mine + 16 + 16 * lane, r[x][2]);
+          put16(mine + 48 + 16 * lane, r[x][3]);
+        }
+      }
+      if (warp == 2 && lane == 0 && local == 1) FL_MARK(46);
+      if (!(a.exp & 64)) named_bar(1 + h, 128);  // DEV 64: no exchange barrier (timing only)
+      if (warp == 2 && lane == 0 && local == 1) FL_MARK(47);
+      if (lane < 3 && q < 3) {
+#pragma unroll
+        for (int x = 0; x < kFlatNfbh; ++x) {
+          const float* nx = rec + ((q + 1) * kFlatNfbh + x) * kFlatXFloats;
+          if (lane == 0) get16(nx, r[x][1]);
+          if (lane < 2) get16(nx + 16 + 16 * lane, r[x][2]);
+          get16(nx + 48 + 16 * lane, r[x][3]);
+        }
+      }
+      if (warp == 2 && lane == 0 && local == 1) FL_MARK(45);
+      const int l1 = (lane + 1) & 31, l2 = (lane + 2) & 31, l3 = (lane + 3) & 31;
+#pragma unroll
+      for (int x = 0; x < kFlatNfbh; ++x) {
+        if (x < nmine) {
+          const int f0 = (h + x * EPW) * 16;
+          float* op = O + (static_cast<int64_t>(n) * a.F + f0) * plane_out + static_cast<int64_t>(hrow) * a.OW + wcol;
+          if (a.F - f0 >= 16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float v = __uint_as_float(r[x][0][i]) + __shfl_sync(0xffffffffu, __uint_as_float(r[x][1][i]), l1) +
+                              __shfl_sync(0xffffffffu, __uint_as_float(r[x][2][i]), l2) +
+                              __shfl_sync(0xffffffffu, __uint_as_float(r[x][3][i]), l3);
+              if (ok) *op = v;
+              op += plane_out;
+            }
+          } else {
+            const int fmax = a.F - f0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float v = __uint_as_float(r[x][0][i]) + __shfl_sync(0xffffffffu, __uint_as_float(r[x][1][i]), l1) +
+                              __shfl_sync(0xffffffffu, __uint_as_float(r[x][2][i]), l2) +
+                              __shfl_sync(0xffffffffu, __uint_as_float(r[x][3][i]), l3);
+              if (ok && i < fmax) *op = v;
+              op += plane_out;
+            }
+          }
+        }
+      }
+      if (warp == 2 && lane == 0 && local < 6) FL_MARK(32 + local);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+size_t flat_smem(const ConvFlatArgs& a, int stages) {
+  return 1024 + static_cast<size_t>(a.nck) * a.T * a.FN * 128 + static_cast<size_t>(stages) * kFlatStage +
+         static_cast<size_t>(2 * kFlatNfbh * kFlatEpw * 4 * kFlatXFloats) * 4 + (2 * stages + 4 + kFlatMaxChunks) * 8 + 16;
+}
+
+}  // namespace
+
+// Host plan: the tap / op table for this W (flat_table.h), tiling, shared-memory ring depth, and
+// whether a compile-time-specialised kernel issues the MMAs (3x3, FN = 64, W >= S + 3: the table
+// depends on W mod 4 only).
+bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a) {
+  if (stride != 1 || C % 32 != 0 || F < 1 || F > 64 || R < 1 || S < 1 || R > H || S > W) return false;
+  if ((static_cast<int64_t>(H) * W) % 4 != 0) return false;  // plane pitch must be 16 B aligned for TMA
+  const int T = R * S;
+  if (T > kFlatMaxTaps) return false;
+  if (static_cast<int64_t>(N) * C > (int64_t{1} << 31) - 1 || static_cast<int64_t>(H) * W > (int64_t{1} << 30) ||
+      static_cast<int64_t>(F) * (H - R + 1) * (W - S + 1) > (int64_t{1} << 31) - 1)
+    return false;
+  a = ConvFlatArgs{};
+  a.N = N, a.C = C, a.H = H, a.W = W, a.F = F, a.R = R, a.S = S;
+  a.OH = H - R + 1, a.OW = W - S + 1;
+  a.FN = (F + 15) / 16 * 16;
+  a.T = T;
+  a.nck = C / 32;
+  a.tb = flat_table(R, S, W, a.FN);
+  if (!a.tb.ok) return false;
+  a.PW = a.OH * W;
+  a.tiles_img = (a.PW + kFlatStep - 1) / kFlatStep;
+  a.total = N * a.tiles_img;
+  a.sms = sms;
+  if (const char* e = dev_env("GENSOR_FLAT_EXP")) a.exp = std::atoi(e);
+  a.ws_bytes = static_cast<size_t>(a.nck) * T * a.FN * 128;
+  a.stages = 0;
+  for (int s = 6; s >= 4; --s)
+    if (flat_smem(a, s) <= 227 * 1024) {
+      a.stages = s;
+      break;
+    }
+  if (a.stages < 4) return false;
+  // specialised issue when the op table equals the class representative's (W mod 4)
+  a.spec = -1;
+  if (R == 3 && S == 3 && a.FN == 64 && W >= S + 3 && a.stages == 4 && !(a.exp & 2048)) {
+    const FlatTable rep = flat_table(R, S, flat_rep_w(S, W & 3), a.FN);
+    bool same = rep.ok && rep.ngroups == a.tb.ngroups && rep.bmask == a.tb.bmask;
+    for (int g = 0; same && g < rep.ngroups; ++g)
+      for (int pass = 0; pass < 2; ++pass) {
+        same = same && rep.grp_op0[pass][g] == a.tb.grp_op0[pass][g] && rep.grp_nop[pass][g] == a.tb.grp_nop[pass][g];
+        for (int o = rep.grp_op0[pass][g]; same && o < rep.grp_op0[pass][g] + rep.grp_nop[pass][g]; ++o)
+          same = rep.op_dcol[o] == a.tb.op_dcol[o] && rep.op_n[o] == a.tb.op_n[o] && rep.op_brow[o] == a.tb.op_brow[o] &&
+                 rep.op_zero[o] == a.tb.op_zero[o];
+      }
+    for (int t = 0; same && t < T; ++t) same = rep.tap_slot[t] == a.tb.tap_slot[t];
+    if (same) a.spec = W & 3;
+  }
+  return true;
+}
+
+void conv_flat_map(const ConvFlatArgs& a, const void* I, CUtensorMap& mapX) {
+  // the NCHW input as {H*W positions, N*C planes}: box {32 positions, 32 planes}
+  const uint64_t dims[2] = {static_cast<uint64_t>(a.H) * a.W, static_cast<uint64_t>(a.N) * a.C};
+  const uint64_t strides[1] = {static_cast<uint64_t>(a.H) * a.W * 4};
+  const uint32_t box[2] = {32, 32};
+  encode_map(&mapX, false, true, I, 2, dims, strides, box, /*atom32=*/true);
+}
+
+void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void* K, void* O, void* ws,
+                      cudaStream_t st, Marks& mk) {
+  if ((reinterpret_cast<uintptr_t>(ws) & 15) != 0) throw Error(Code::Cuda, "conv_flat: workspace alignment");
+  const int grid = std::min(a.total, a.sms);
+  const size_t smem = flat_smem(a, a.stages);
+  mk.mark(st);
+  const int nf = a.FN * (a.C / 4) * a.T;
+  if (!(a.exp & 4096)) {  // DEV 4096: keep the previous execute's bank image (timing only)
+    k_flat_filters<<<(nf + 127) / 128, 128, 0, st>>>(static_cast<const float*>(K), static_cast<uint8_t*>(ws), a);
+    check_cuda(cudaGetLastError(), "conv_flat filter launch");
+    count_launch();
+  }
+  auto launch = [&](auto kern) {
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "conv_flat smem attribute");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32 * (2 + 4 * kFlatEpw));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, mapX, a, static_cast<const uint8_t*>(ws), static_cast<float*>(O)),
+               "conv_flat launch");
+    count_launch();
+  };
+  switch (a.spec) {
+    case 0: launch(k_conv_flat<4, FlatSpec<3, 3, 0, 64>>); break;
+    case 1: launch(k_conv_flat<4, FlatSpec<3, 3, 1, 64>>); break;
+    case 2: launch(k_conv_flat<4, FlatSpec<3, 3, 2, 64>>); break;
+    case 3: launch(k_conv_flat<4, FlatSpec<3, 3, 3, 64>>); break;
+    default:
+      switch (a.stages) {
+        case 4: launch(k_conv_flat<4, void>); break;
+        case 5: launch(k_conv_flat<5, void>); break;
+        case 6: launch(k_conv_flat<6, void>); break;
+        default: throw Error(Code::Unsupported, "conv_flat: stage count");
+      }
+  }
+  mk.mark(st);
+}
+
+}  // namespace gb::dev

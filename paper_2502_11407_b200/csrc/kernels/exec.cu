@@ -35,7 +35,7 @@ void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxe
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 
-enum class Family { Generic, GemmTc, ConvTc, ConvGemm, Stream };
+enum class Family { Generic, GemmTc, ConvTc, ConvGemm, ConvFlat, Stream };
 
 // Tensor maps of one (inputs, output, workspace) pointer tuple. Encoding is pure host work, but
 // at a few microseconds per execute it would show on the microsecond-scale ops, so the handle
@@ -47,6 +47,7 @@ struct CallMaps {
   GemmTcMaps g;
   ConvTcMaps c;
   CUtensorMap w;
+  CUtensorMap x;  // conv_flat: the caller's NCHW input as {H*W, N*C}
 };
 constexpr int kMapCache = 4;
 
@@ -70,6 +71,7 @@ struct Kernel {
   GemmTcArgs gemm;
   ConvTcArgs conv;
   ConvGemmArgs cgemm;
+  ConvFlatArgs flat;
   StreamArgs stream;
   int launches = 1;
   std::vector<std::string> launch_names{"generic_simt"};
@@ -294,6 +296,22 @@ bool conv1x1_gemm_ok(const OpDesc& op, bool bf16) {
                                                                      static_cast<int>(op.param("C")), 4);
 }
 
+// conv_flat (tf32, stride 1, C % 32 == 0, F <= 64, H*W % 4 == 0): flattened NCHW planes read in
+// place by TMA, one launch (no NHWC copy, no filter pre-pass)
+bool conv_flat_ok(const OpDesc& op, bool bf16, int sms, ConvFlatArgs* out) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16 || op.batch != 1) return false;
+  if (dev_env("GENSOR_CONV_FLAT") && dev_env("GENSOR_CONV_FLAT")[0] == '0') return false;  // A/B
+  ConvFlatArgs a;
+  if (!conv_flat_plan(static_cast<int>(op.param("N")), static_cast<int>(op.param("C")),
+                      static_cast<int>(op.param("H")), static_cast<int>(op.param("W")),
+                      static_cast<int>(op.param("F")), static_cast<int>(op.param("R")),
+                      static_cast<int>(op.param("S")), static_cast<int>(op.stride), sms, a))
+    return false;
+  if (a.R < 2 && a.S < 2) return false;  // 1x1: gemm_tc / conv_gemm
+  if (out) *out = a;
+  return true;
+}
+
 // General implicit-GEMM conv (tf32): any stride / window / channel count.
 bool conv_gemm_ok(const OpDesc& op, bool bf16) { return op.kind == Kind::Conv2d && op.dtype_bytes == 4 && !bf16; }
 
@@ -408,6 +426,24 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
              << ",\"BM\":128,\"BN\":" << g.BN << ",\"BK_bytes\":128,\"stages\":" << gemm_tc_stages(g)
              << ",\"tiles\":" << tiles(g.BN) << ",\"grid\":" << std::min<int64_t>(tiles(g.BN), sms)
              << ",\"block\":192,\"persistent\":true,\"cluster_n\":" << g.cs << "}";
+        } else if (op.kind == Kind::Conv2d && conv_flat_ok(op, bf16, sms, &k->flat)) {
+          k->family = Family::ConvFlat;
+          k->launch_names = {"conv_flat"};
+          const ConvFlatArgs& c = k->flat;
+          k->launches = 2;  // bank conversion + conv (programmatic dependent launch), timed as one span
+          k->ws_bytes = c.ws_bytes;
+          pi << "{\"family\":\"conv_flat\",\"M_tile\":\"128 wide positions of one image (124 outputs)\",\"FN\":"
+             << c.FN << ",\"tap_groups\":[";
+          for (int g = 0; g < c.tb.ngroups; ++g) {
+            pi << (g ? "," : "") << "{\"a\":" << (c.tb.group_o[g] & ~3) << ",\"umma\":[";
+            for (int o = c.tb.grp_op0[1][g]; o < c.tb.grp_op0[1][g] + c.tb.grp_nop[1][g]; ++o)
+              pi << (o > c.tb.grp_op0[1][g] ? "," : "") << "{\"b0\":" << c.tb.op_dcol[o] / c.FN << ",\"N\":" << c.tb.op_n[o]
+                 << "}";
+            pi << "]}";
+          }
+          pi << "],\"tiles\":" << c.total << ",\"grid\":" << std::min(c.total, sms) << ",\"stages\":" << c.stages
+             << ",\"mma_issue\":\"" << (c.spec >= 0 ? "specialised (3x3, W mod 4)" : "table-driven")
+             << "\",\"block\":576,\"launches\":2,\"A\":\"MN-major TMA boxes straight from the NCHW input\",\"B\":\"bank image converted by a PDL-chained launch, bulk-copied, resident\"}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16) &&
                    !(dev_env("GENSOR_CONV_FAMILY") && std::string(dev_env("GENSOR_CONV_FAMILY")) == "gemm" &&
                      !bf16)) {  // developer switch: A/B the two conv families on one shape
@@ -630,6 +666,9 @@ void call_maps(const Kernel* k, const void* const* d_in, int n_in, void* d_out, 
     case Family::ConvGemm:
       conv_gemm_map(k->cgemm, ws, fresh.w);
       break;
+    case Family::ConvFlat:
+      conv_flat_map(k->flat, d_in[0], fresh.x);
+      break;
     default:
       break;
   }
@@ -684,6 +723,12 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
       CallMaps m;
       call_maps(k, d_in, n_in, d_out, ws, m);
       launch_conv_gemm(k->cgemm, m.w, d_in[0], d_in[1], d_out, ws, st, mk);
+      break;
+    }
+    case Family::ConvFlat: {
+      CallMaps m;
+      call_maps(k, d_in, n_in, d_out, ws, m);
+      launch_conv_flat(k->flat, m.x, d_in[1], d_out, ws, st, mk);
       break;
     }
     case Family::Stream:

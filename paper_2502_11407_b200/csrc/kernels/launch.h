@@ -3,6 +3,8 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include "flat_table.h"
 #include <stddef.h>
 
 #include "plan.h"
@@ -87,6 +89,24 @@ bool conv_s2d_supported(int C, int F, int R, int S, int stride, bool bf16);
 size_t conv_tc_smem_need(int C, int F, int R, int S, bool bf16);
 void launch_conv_tc(const ConvTcArgs& a, const ConvTcMaps& m, const void* I, const void* K, void* O, void* ws,
                     cudaStream_t st, Marks& mk);
+
+// ---- flattened-plane stride-1 tf32 conv2d reading NCHW in place, one launch (conv_flat.cu) ----
+struct ConvFlatArgs {
+  int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
+  int FN = 0;    // filter rows per tap slot (F rounded up to 16)
+  int T = 0;     // taps R*S
+  int nck = 0;   // 32-channel chunks
+  int PW = 0;    // wide positions per image (OH * W)
+  int tiles_img = 0, total = 0, stages = 0, sms = 148;
+  int spec = -1; // compile-time-specialised MMA issue (3x3, FN 64: W mod 4), -1 = table-driven
+  int exp = 0;   // developer experiments (DEV build, GENSOR_FLAT_EXP): 0 in the product
+  size_t ws_bytes = 0;  // bank image W' (workspace), rewritten by every execute
+  FlatTable tb;         // taps, groups and the MMA op table for this W (flat_table.h)
+};
+bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a);
+void conv_flat_map(const ConvFlatArgs& a, const void* I, CUtensorMap& mapX);
+void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void* K, void* O, void* ws,
+                      cudaStream_t st, Marks& mk);
 
 // ---- HBM-streaming family (stream.cu): gemv / softmax / avgpool2d / dwconv2d ----
 enum class StreamKind : int { Gemv, Softmax, AvgPool, DwConv };

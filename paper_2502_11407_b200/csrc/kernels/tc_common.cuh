@@ -54,6 +54,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Waiting with a suspend-time hint: the thread sleeps in the barrier unit (up to `ns`) instead
+// of re-polling shared memory; for warps that wait long (epilogue, producer) so their polling
+// does not compete with the tensor core for shared-memory cycles.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 2000) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra.uni DONE_%=;\n\t"
+      "bra.uni WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
 // ---- TMA (cp.async.bulk.tensor), completion signalled on an mbarrier ----------------------
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -18,7 +18,8 @@ from oracle import oracle as O  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 OPS = {
-    "conv_ns": {"kind": "conv2d", "I": [4, 64, 30, 30], "K": [64, 64, 3, 3], "S": 1},
+    "conv_flat": {"kind": "conv2d", "I": [4, 64, 30, 30], "K": [64, 64, 3, 3], "S": 1},
+    "conv_ns": {"kind": "conv2d", "I": [4, 48, 30, 30], "K": [64, 48, 3, 3], "S": 1},
     "conv_gemm": {"kind": "conv2d", "I": [3, 32, 19, 19], "K": [96, 32, 3, 3], "S": 2},
     "conv_tc": {"kind": "conv2d", "I": [2, 128, 14, 14], "K": [128, 128, 3, 3], "S": 1},
     "gemm_tc": {"kind": "gemm", "M": 384, "K": 256, "N": 320},
@@ -58,7 +59,7 @@ def test_one_handle_two_streams_concurrently(family):
         assert family != "gemm_tc"
 
 
-@pytest.mark.parametrize("family", ["conv_ns", "conv_gemm", "conv_tc"])
+@pytest.mark.parametrize("family", ["conv_flat", "conv_ns", "conv_gemm", "conv_tc"])
 def test_caller_workspace_and_filter_change(family):
     doc = OPS[family]
     op, k, xs, nout = _setup(doc, seed=2)

@@ -114,7 +114,28 @@ CONVS = [
     {"kind": "conv2d", "I": [3, 128, 14, 18], "K": [128, 128, 3, 3], "S": 1},  # filters streamed per stage
     {"kind": "conv2d", "I": [2, 96, 11, 13], "K": [100, 96, 3, 3], "S": 1},   # streamed, ragged F / C
     {"kind": "conv2d", "I": [2, 3, 16, 18], "K": [32, 3, 3, 3], "S": 1},      # C = 3: no 16 B NHWC rows
+    # conv_flat (flattened NCHW planes, TMA in place): tap offset classes / runs / bank shapes
+    {"kind": "conv2d", "I": [2, 32, 12, 14], "K": [48, 32, 3, 3], "S": 1},    # W = 14: split runs, F = 48
+    {"kind": "conv2d", "I": [3, 64, 16, 16], "K": [64, 64, 3, 3], "S": 1},    # W % 4 == 0: block 3 unused
+    {"kind": "conv2d", "I": [1, 32, 9, 12], "K": [20, 32, 2, 2], "S": 1},     # 4 taps, FN 32 > F
+    {"kind": "conv2d", "I": [2, 32, 30, 30], "K": [64, 32, 3, 3], "S": 1},    # 7 tiles per image
+    {"kind": "conv2d", "I": [1, 32, 20, 24], "K": [32, 32, 5, 5], "S": 1},    # 25 taps, runs of 4
+    {"kind": "conv2d", "I": [1, 96, 10, 10], "K": [16, 96, 3, 3], "S": 1},    # 3 chunks, FN = 16
 ]
+
+
+def flat_ok(doc):
+    """conv_flat's envelope (kernels/conv_flat.cu conv_flat_plan): tf32, stride 1, C % 32 == 0,
+    F <= 64, H*W % 4 == 0, a window, and the resident bank + 4 A stages fit shared memory."""
+    N, C, H, W = doc["I"]
+    F, _, R, S = doc["K"]
+    if doc.get("S", 1) != 1 or C % 32 or F > 64 or (H * W) % 4 or (R == 1 and S == 1):
+        return False
+    fn = (F + 15) // 16 * 16
+    nfb = fn // 16
+    nfbh = (nfb + 1) // 2
+    smem = 1024 + (C // 32) * R * S * fn * 128 + 4 * 16384 + 2 * nfbh * 2 * 4 * 96 * 4 + 12 * 8 + 16
+    return smem <= 227 * 1024
 
 
 @pytest.mark.parametrize("doc", CONVS, ids=lambda d: json.dumps(d["I"] + d["K"]))
@@ -139,6 +160,8 @@ def test_conv_tc(doc, variant, tol):
     if (variant == "tc_tf32" and doc["K"][2] == 1 and doc["K"][3] == 1 and doc["I"][1] % 4 == 0 and P % 4 == 0
             and (P >= 512 or P % 128 == 0)):
         want = "gemm_tc"    # 1x1 stride 1: batched GEMM O[n] = K . I[n] on the NCHW tensors
+    elif variant == "tc_tf32" and flat_ok(doc):
+        want = "conv_flat"  # flattened NCHW planes straight through TMA, one launch
     elif variant == "tc_tf32" and (doc["K"][2] == 1 or C % 4):
         want = "conv_gemm"  # other 1x1, and channel counts without 16 B NHWC rows: in-place implicit GEMM
     elif variant == "tc_tf32" and S <= 4 and S * fn <= 256 and C % 4 == 0:

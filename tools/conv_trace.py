@@ -32,6 +32,7 @@ def timed(n=30):
     ts = []
     for _ in range(n):
         flush.zero_()
+        torch.cuda._sleep(80_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         k.execute(xs, out)
@@ -41,7 +42,9 @@ def timed(n=30):
     return statistics.median(ts)
 
 
-for mode in (None, "prepass", "conv"):
+if k.info["plan"]["family"] == "conv_flat":
+    print(f"conv_flat step (events, L2 flushed): {timed():.2f} us", flush=True)
+for mode in (() if k.info["plan"]["family"] == "conv_flat" else (None, "prepass", "conv")):
     if mode:
         os.environ["GENSOR_CONV_SKIP"] = mode
     else:
@@ -49,7 +52,8 @@ for mode in (None, "prepass", "conv"):
     print(f"skip={mode}: {timed():.2f} us", flush=True)
 os.environ.pop("GENSOR_CONV_SKIP", None)
 lib = g.gensor.lib()
-fn = lib.gensor_dev_conv_trace
+fam = k.info["plan"]["family"]
+fn = lib.gensor_dev_flat_trace if fam == "conv_flat" else lib.gensor_dev_conv_trace
 fn.argtypes = [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 buf = (ctypes.c_longlong * (160 * 64))()
 flush.zero_()
@@ -74,4 +78,8 @@ print("first MMA start: median", np.median(first_mma), "griddep wait", np.median
       "filters ready", np.median([r[3] for r in rows]))
 mma = [r[5][i] - r[4][i] for r in rows for i in range(r[1])]
 epi = [r[7][i] - r[6][i] for r in rows for i in range(r[1])]
+if fam == "conv_flat":
+    e = rel[:, 24 + 1]
+    print("epilogue tile 1 (cycles from acc_full): blocks read", np.median(rel[:, 44] - e), "published", np.median(rel[:, 46] - e), "barrier", np.median(rel[:, 47] - e), "exchanged",
+          np.median(rel[:, 45] - e), "done", np.median(rel[:, 33] - e))
 print("MMA issue->commit per tile: median", np.median(mma), " epilogue per tile: median", np.median(epi))
