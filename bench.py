@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -493,7 +494,7 @@ def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
     from paper_2502_11407_b200 import sequences as S
 
     seq = S.sharded(name, ws)
-    kern, bufs, con = {}, {}, {}
+    kern, con = {}, {}
     gen = torch.Generator(device=device)
     gen.manual_seed(0)
     for key, spec_op in S.distinct(seq).items():
@@ -501,16 +502,31 @@ def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
         t0 = time.perf_counter()
         sched = g.optimize(op, hw, g.EngineConfig(seed=0, mode="b200"))
         con[key] = time.perf_counter() - t0
-        k = g.Kernel(op, sched, 0, "auto")
-        xs, out = make_inputs(op, {"op": spec_op}, gen, torch, device)
-        kern[key] = (op, k)
-        bufs[key] = (xs, out)
+        kern[key] = (op, g.Kernel(op, sched, 0, "auto"))
     keys = [json.dumps(sp, sort_keys=True) for _, sp in seq]
+    # per-instance buffers, chained: an op whose first input has the element count and dtype of the
+    # previous op's output reads that output buffer (ResNet: conv3 -> next conv1 / conv2 -> conv3;
+    # GPT-2: qk -> softmax -> pv -> proj -> fc1 -> fc2 -> next qkv); other inputs are synthetic.
+    # Weights are U(-1,1) * sqrt(3 / reduction) so chained activations keep unit scale.
+    bufs, chained = [], 0
+    for i, key in enumerate(keys):
+        op, _ = kern[key]
+        xs, out = make_inputs(op, {"op": seq[i][1]}, gen, torch, device)
+        red = {"gemm": "K", "conv2d": None}.get(seq[i][1]["kind"])
+        if red == "K":
+            xs[1].mul_(math.sqrt(3.0 / seq[i][1]["K"]))
+        elif seq[i][1]["kind"] == "conv2d":
+            kk = seq[i][1]["K"]
+            xs[1].mul_(math.sqrt(3.0 / (kk[1] * kk[2] * kk[3])))
+        if bufs and bufs[-1][1].numel() == xs[0].numel() and bufs[-1][1].dtype == xs[0].dtype:
+            xs[0] = bufs[-1][1]
+            chained += 1
+        bufs.append((xs, out))
     stream = torch.cuda.current_stream(device)
 
     def step():
-        for key in keys:
-            kern[key][1].execute(bufs[key][0], bufs[key][1], stream)
+        for i, key in enumerate(keys):
+            kern[key][1].execute(bufs[i][0], bufs[i][1], stream)
 
     for _ in range(warmup):
         step()
@@ -519,7 +535,7 @@ def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(keys) + 1)]
     ev[0].record(stream)
     for i, key in enumerate(keys):
-        kern[key][1].execute(bufs[key][0], bufs[key][1], stream)
+        kern[key][1].execute(bufs[i][0], bufs[i][1], stream)
         ev[i + 1].record(stream)
     ev[-1].synchronize()
     per_op = {}
@@ -543,8 +559,8 @@ def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=side):
             cap = torch.cuda.current_stream(device)
-            for key in keys:
-                kern[key][1].execute(bufs[key][0], bufs[key][1], cap)
+            for i, key in enumerate(keys):
+                kern[key][1].execute(bufs[i][0], bufs[i][1], cap)
         per_step = g.launch_count() - c0
         torch.cuda.synchronize(device)
     except Exception as exc:  # pragma: no cover - driver without graph support for these launches
@@ -566,21 +582,20 @@ def run_sequence(g, torch, name, hw, steps, warmup, device, ws, flush):
     launches = per_step * steps if graph is not None else g.launch_count() - n0
     flops = sum(kern[k][0].flops for k in keys)
     # e2e: the shard's input batch from pinned host memory, the final output back
-    first, last = keys[0], keys[-1]
-    hin = bufs[first][0][0].cpu().pin_memory()
-    hout = torch.empty(bufs[last][1].numel(), dtype=bufs[last][1].dtype).pin_memory()
+    hin = bufs[0][0][0].cpu().pin_memory()
+    hout = torch.empty(bufs[-1][1].numel(), dtype=bufs[-1][1].dtype).pin_memory()
     e2e_ms = []
     for _ in range(max(3, steps // 2)):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        bufs[first][0][0].copy_(hin, non_blocking=True)
+        bufs[0][0][0].copy_(hin, non_blocking=True)
         step()
-        hout.copy_(bufs[last][1], non_blocking=True)
+        hout.copy_(bufs[-1][1], non_blocking=True)
         e.record(stream)
         e.synchronize()
         e2e_ms.append(s.elapsed_time(e))
     return dict(seq=seq, step_ms=step_ms, e2e_ms=e2e_ms, per_op=per_op, launches=launches, flops=flops,
-                graph=graph is not None,
+                graph=graph is not None, chained=chained,
                 construct_s=sum(con.values()), n_distinct=len(con), h2d=hin.numel() * hin.element_size(),
                 d2h=hout.numel() * hout.element_size())
 
@@ -614,6 +629,7 @@ def sequence_line(args, res, ws, peaks, tf32, clk, total_ms, e2e_ms):
                    "launch": "CUDA graph of the step (captured once, replayed per step)" if res.get("graph")
                    else "eager stream launches",
                    "distinct_ops": res["n_distinct"],
+                   "chained_inputs": res.get("chained"),
                    "parallelism": f"batch-sharded over {ws} GPU(s), one process per GPU, no collective",
                    "l2": "flushed between steps (256 MiB write outside the events)"},
         "roofline": {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
@@ -843,6 +859,28 @@ def run_ours(args):
                 suite[wname] = {"error": str(exc)[:300]}
             torch.cuda.empty_cache()
 
+    sequences = {}
+    if ws == 1 and not args.no_sequences:
+        # configs[4] on one GPU, summarised into the default line (the full lines: --workload resnet50|gpt2)
+        for sname in ("resnet50", "gpt2"):
+            try:
+                sargs = argparse.Namespace(**{**vars(args), "workload": sname, "steps": 5, "warmup": 2})
+                with ClockSampler(local) as sclk:
+                    sres = run_sequence(g, torch, sname, hw, sargs.steps, sargs.warmup, device, ws, flush)
+                sl = sequence_line(sargs, sres, ws, peaks, tf32, sclk, sum(sres["step_ms"]),
+                                   statistics.mean(sres["e2e_ms"]))
+                sequences[sname] = {k: sl[k] for k in ("value", "unit", "ms_per_step", "steps", "gpu_launches",
+                                                       "construction_s")}
+                sequences[sname]["e2e"] = {k: sl["e2e"][k] for k in ("value", "unit", "ms_per_step")}
+                sequences[sname]["roofline_top_op"] = {k: sl["roofline"][k] for k in ("kernel", "achieved", "peak",
+                                                                                      "frac", "share_of_step")}
+                sequences[sname]["config"] = {k: sl["config"][k] for k in ("workload", "ops", "distinct_ops",
+                                                                          "chained_inputs", "launch")}
+                del sres
+            except Exception as exc:  # keep the headline line even if a sequence fails
+                sequences[sname] = {"error": str(exc)[:300]}
+            torch.cuda.empty_cache()
+
     base = None
     ref_con = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -880,6 +918,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "cpu_baseline": base,
         "suite": suite or None,
+        "sequences": sequences or None,
     }
     print(json.dumps(line), flush=True)
     if pg:
@@ -940,6 +979,8 @@ def main():
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--suite", default=",".join(SUITE_DEFAULT))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sequences", action="store_true",
+                    help="skip the ResNet-50 / GPT-2 sequence summaries of the default line")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--strong", action="store_true",
                     help="N>1: split the BASELINE batch N ways (default: one BASELINE-sized shard per rank)")
