@@ -309,7 +309,8 @@ def flush_l2(torch, flush):
     torch.cuda._sleep(80_000)
 
 
-def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=None):
+def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=(None, None)):
+    traffic, traffic_detail = traffic
     name, ms = max(res["launch_ms"].items(), key=lambda kv: statistics.mean(kv[1]))
     avg = statistics.mean(ms) / 1e3
     if spec["bound"] == "tensor":
@@ -330,15 +331,23 @@ def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=None):
              "traffic": traffic, "kernel": name, "peak_source": f"hbm copy, {peaks['source']}",
              "share_of_step": statistics.mean(ms) / statistics.mean(res["step_ms"])}
     r["algorithmic_per_launch"] = res["flops"] if spec["bound"] == "tensor" else res["bytes"]
+    r["traffic_detail"] = traffic_detail
+    r["algorithmic_bytes"] = res["bytes"]
     return r
 
 
 def ncu_traffic(workload):
+    """DRAM bytes (read + write) of every launch of one execute, from ncu (profiles/ncu_traffic.json,
+    tools/gpu_traffic.sh), and the detail: output lines still dirty in L2 at kernel end are not in
+    dram_write, so the store traffic the kernels sent to L2 is listed beside it."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get(workload)
-    return None
+            t = json.load(f)
+        if workload in t:
+            det = t.get(workload + "_detail", {})
+            return t[workload], {k: det.get(k) for k in ("dram_read", "dram_write", "l2_write_from_sm", "launches")}
+    return None, None
 
 
 def _pow2(x: int) -> int:
