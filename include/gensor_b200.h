@@ -112,7 +112,8 @@ int gensor_op_info(const gensor_op* op, char* buf, size_t cap, size_t* need);
 /* ---- hardware model: replaces HardwareSpec::load_text (hardware.hpp:31) ------------------ */
 int gensor_hw_load(const char* json, gensor_hw** out);
 /* B200 model from the live device query + measured peaks (JSON text of MEASURED_PEAKS.json or
- * NULL for the built-in defaults). New: the reference has no device model. */
+ * NULL for the built-in defaults); device < 0 uses the nominal B200 limits without a device
+ * query (construction on a host without a GPU). New: the reference has no device model. */
 int gensor_hw_b200(int device, const char* measured_peaks_json, gensor_hw** out);
 void gensor_hw_free(gensor_hw* hw);
 int gensor_hw_json(const gensor_hw* hw, char* buf, size_t cap, size_t* need);

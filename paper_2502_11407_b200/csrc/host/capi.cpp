@@ -249,7 +249,9 @@ int gensor_hw_load(const char* json, gensor_hw** out) {
 int gensor_hw_b200(int device, const char* peaks, gensor_hw** out) {
   if (!out) return fail(GENSOR_EINVALID, "null argument");
   return guarded([&]() -> int {
-    gb::DeviceLimits lim = gb::dev::query(device);
+    // device < 0: the nominal B200 limits (hw.hpp defaults) without a device query — construction
+    // in B200 mode on a host without a GPU (CPU tests, offline schedule caches)
+    gb::DeviceLimits lim = device < 0 ? gb::DeviceLimits{} : gb::dev::query(device);
     if (peaks && *peaks) {
       gb::json::Value p = gb::json::parse(peaks);
       if (const auto* v = p.find("hbm_gbs")) lim.hbm_bytes_per_s = v->as_double() * 1e9;
