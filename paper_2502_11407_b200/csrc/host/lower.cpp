@@ -162,7 +162,8 @@ std::string plan_json(const GenericPlan& p) {
   os << "{\"family\":\"generic\",\"grid\":" << grid << ",\"block\":" << p.block << ",\"slots\":" << p.slots
      << ",\"acc\":" << p.acc << ",\"acc_chunks\":" << p.acc_chunks << ",\"rounds\":" << p.rounds
      << ",\"n_chunks\":" << p.n_chunks << ",\"chunk_len\":" << p.chunk_len << ",\"staged\":" << p.staged
-     << ",\"smem_bytes\":" << p.smem_bytes << ",\"block_tile\":[";
+     << ",\"smem_bytes\":" << p.smem_bytes
+     << ",\"fast\":\"" << (p.fast == 1 ? "gemm" : p.fast == 2 ? "gemv" : "none") << "\",\"block_tile\":[";
   for (int i = 0; i < p.nsp; ++i) os << (i ? "," : "") << p.B[i];
   os << "],\"thread_tile\":[";
   for (int i = 0; i < p.nsp; ++i) os << (i ? "," : "") << p.T[i];

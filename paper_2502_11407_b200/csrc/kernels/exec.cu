@@ -324,6 +324,28 @@ int resolve_variant(const OpDesc& op, int variant) {
   return 1;
 }
 
+// simt_f32 fast paths (kernels/generic.cu k_simt_gemm / k_simt_gemv): the same plan — tiles,
+// vthreads, ascending single-axis reduce — executed by register-tiled kernels when its shape fits
+// their envelope (one round of thread slots, power-of-two thread tiles up to 8, shared memory).
+void simt_fast_path(const OpDesc& op, GenericPlan& p, int64_t optin) {
+  if (dev_env("GENSOR_SIMT_FAST") && dev_env("GENSOR_SIMT_FAST")[0] == '0') return;  // A/B
+  auto tile_ok = [](int t) { return t == 1 || t == 2 || t == 4 || t == 8; };
+  if (p.rounds != 1 || p.nred != 1) return;
+  if (op.kind == Kind::Gemm && p.nsp == 2 && tile_ok(p.T[0]) && tile_ok(p.T[1])) {
+    const int64_t bm = p.B[0], bn = p.B[1], bk = p.chunk_tile[0], pad = 0;  // A rows swizzled, no pad
+    const int64_t smem = (bm * bk + bk * bn) * 4;
+    if (smem > optin) return;
+    p.fast = 1;
+    p.fast_pad = static_cast<int32_t>(pad);
+    p.smem_bytes = static_cast<int32_t>(smem);
+  } else if (op.kind == Kind::Gemv && p.nsp == 1 && tile_ok(p.T[0]) && op.dtype_bytes == 4) {
+    const int64_t n = p.ext[p.red[0]];
+    p.fast = 2;
+    p.fast_pad = n * 4 <= std::min<int64_t>(optin, 96 * 1024) ? 1 : 0;  // x staged in shared memory
+    p.smem_bytes = p.fast_pad ? static_cast<int32_t>(n * 4) : 0;
+  }
+}
+
 int current_device_sms(int* optin_smem) {
   int dev = 0, sms = 0, optin = 0;
   check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -374,6 +396,7 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
         k->f64 = k->variant == 0;
         k->family = Family::Generic;
         k->gplan = lower_generic(op, s, generic_max_width(k->f64), op.dtype_bytes, optin);
+        if (!k->f64) simt_fast_path(op, k->gplan, optin);
         pi << plan_json(k->gplan);
         break;
       }

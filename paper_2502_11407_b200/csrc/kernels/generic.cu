@@ -13,6 +13,9 @@
 #include "common.cuh"
 #include "launch.h"
 #include "plan.h"
+#include "tc_common.cuh"
+
+#include <type_traits>
 
 namespace gb::dev {
 
@@ -169,6 +172,280 @@ __global__ void __launch_bounds__(256) k_generic(const GenericPlan p, const In* 
   }
 }
 
+// ---- register-tiled fast paths of the same plans (simt_f32) --------------------------------
+// The program is the plan's: CTA = level-1 spatial tile, thread = level-L thread tile split into
+// vthread slices (slice e of a thread covers (e / per) * (B / V) + th * per + e % per), the reduce
+// axis walked in ascending order through level-1 chunks staged in shared memory — for a single
+// reduce axis that IS the interpreter's order (chunks, then level-2.. digits, then scalars), so
+// outputs equal k_generic<float>'s. What changes is mechanical: compile-time thread tiles, the A
+// chunk staged k-major so a thread's rows are adjacent words (float4 loads when a slice holds >= 4),
+// no index decoding in the k loop.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <typename In, int TM, int TN>
+__global__ void __launch_bounds__(256) k_simt_gemm(const GenericPlan p, const In* __restrict__ A,
+                                                   const In* __restrict__ Bm, In* __restrict__ C) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int BM = p.B[0], BN = p.B[1], BK = p.chunk_tile[0];
+  // A chunk row-major [BM][BK], 16 B granules of row mm XOR-swizzled by ((mm >> 3) & 7): a warp's
+  // TM-row reads (4 row groups x 8 rows apart) hit distinct banks, and 16 B copies stay aligned
+  float* As = reinterpret_cast<float*>(smem_raw);
+  float* Bs = As + BM * BK;  // [BK][BN]
+  const int am = p.sp[0], an = p.sp[1], ak = p.red[0];
+  const int64_t M = p.ext[am], N = p.ext[an], K = p.ext[ak];
+  const int64_t b = blockIdx.y;
+  A += b * p.batch_stride[0];
+  Bm += b * p.batch_stride[1];
+  C += b * p.batch_stride[2];
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x / p.tiles[1]) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x % p.tiles[1]) * BN;
+  const int sn = BN / TN;
+  const bool active = static_cast<int>(threadIdx.x) < p.slots;
+  const int thm = active ? threadIdx.x / sn : 0, thn = active ? threadIdx.x % sn : 0;
+  const int perm = TM / p.V[0], pern = TN / p.V[1];
+  const int strm = BM / p.V[0], strn = BN / p.V[1];
+  int ra[TM], fx[TM], rn[TN];
+#pragma unroll
+  for (int e = 0; e < TM; ++e) {
+    const int mm = (e / perm) * strm + thm * perm + e % perm;
+    ra[e] = mm * BK;
+    fx[e] = BK >= 32 ? ((mm >> 3) & 7) << 2 : 0;
+  }
+#pragma unroll
+  for (int e = 0; e < TN; ++e) rn[e] = (e / pern) * strn + thn * pern + e % pern;
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+  const int64_t a_m = p.coef[0][am], a_k = p.coef[0][ak], b_k = p.coef[1][ak], b_n = p.coef[1][an];
+  const bool bvec = pern % 4 == 0 && BN % 4 == 0;
+  // 16 B asynchronous copies when both operands are fp32 with unit-stride, 16 B-aligned rows
+  const bool v16 = sizeof(In) == 4 && a_k == 1 && b_n == 1 && (a_m & 3) == 0 && (b_k & 3) == 0 && (n0 & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(Bm) & 15) == 0 &&
+                   BK % 4 == 0 && BN % 4 == 0;
+  const int kshift = __ffs(BK) - 1, nshift = __ffs(BN) - 1;  // level-1 tiles are powers of two
+  auto swz = [&](int mm, int kk) { return mm * BK + (kk ^ (BK >= 32 ? ((mm >> 3) & 7) << 2 : 0)); };
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    const int kc = static_cast<int>(K - k0 < BK ? K - k0 : BK);
+    __syncthreads();  // the previous chunk is consumed
+    if constexpr (sizeof(In) == 4) {
+      if (v16) {
+        // A: BM rows x BK/4 granules; B: BK rows x BN/4 granules (zero-filled out of range)
+        for (int e = threadIdx.x; e < (BM * BK) >> 2; e += blockDim.x) {
+          const int mm = (4 * e) >> kshift, kk = (4 * e) & (BK - 1);
+          const int64_t krem = kc - kk;
+          const int bytes = m0 + mm < M ? static_cast<int>(krem >= 4 ? 16 : krem > 0 ? 4 * krem : 0) : 0;
+          cp_async16(As + swz(mm, kk), bytes ? A + (m0 + mm) * a_m + (k0 + kk) : A, bytes);
+        }
+        for (int e = threadIdx.x; e < (BK * BN) >> 2; e += blockDim.x) {
+          const int kk = (4 * e) >> nshift, nn = (4 * e) & (BN - 1);
+          const int64_t nrem = N - (n0 + nn);
+          const int bytes = kk < kc ? static_cast<int>(nrem >= 4 ? 16 : nrem > 0 ? 4 * nrem : 0) : 0;
+          cp_async16(Bs + kk * BN + nn, bytes ? Bm + (k0 + kk) * b_k + (n0 + nn) : Bm, bytes);
+        }
+      } else {
+        for (int e = threadIdx.x; e < BM * BK; e += blockDim.x) {  // coalesced along k
+          const int mm = e >> kshift, kk = e & (BK - 1);
+          const bool ok = kk < kc && m0 + mm < M;
+          cp_async4(As + swz(mm, kk), ok ? A + (m0 + mm) * a_m + (k0 + kk) * a_k : A, ok);
+        }
+        for (int e = threadIdx.x; e < BK * BN; e += blockDim.x) {
+          const int kk = e >> nshift, nn = e & (BN - 1);
+          const bool ok = kk < kc && n0 + nn < N;
+          cp_async4(Bs + kk * BN + nn, ok ? Bm + (k0 + kk) * b_k + (n0 + nn) * b_n : Bm, ok);
+        }
+      }
+      cp_async_wait_all();
+    } else {
+      for (int e = threadIdx.x; e < BM * BK; e += blockDim.x) {
+        const int mm = e >> kshift, kk = e & (BK - 1);
+        As[swz(mm, kk)] = kk < kc && m0 + mm < M ? to_f32(A[(m0 + mm) * a_m + (k0 + kk) * a_k]) : 0.0f;
+      }
+      for (int e = threadIdx.x; e < BK * BN; e += blockDim.x) {
+        const int kk = e >> nshift, nn = e & (BN - 1);
+        Bs[kk * BN + nn] = kk < kc && n0 + nn < N ? to_f32(Bm[(k0 + kk) * b_k + (n0 + nn) * b_n]) : 0.0f;
+      }
+    }
+    __syncthreads();
+    if (!active) continue;
+    auto step = [&](int kk, const int (&abase)[TM], int r) {
+      float a[TM], bv[TN];
+#pragma unroll
+      for (int e = 0; e < TM; ++e) a[e] = As[abase[e] + r];
+      if (bvec) {
+#pragma unroll
+        for (int e = 0; e < TN; e += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(Bs + kk * BN + rn[e]);
+          bv[e] = x.x, bv[e + 1] = x.y, bv[e + 2] = x.z, bv[e + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < TN; ++e) bv[e] = Bs[kk * BN + rn[e]];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], bv[j], acc[i][j]);
+    };
+    int kq = 0;
+    for (; kq + 4 <= kc; kq += 4) {  // ascending k; the swizzle is constant inside a 16 B granule
+      int abase[TM];
+#pragma unroll
+      for (int e = 0; e < TM; ++e) abase[e] = ra[e] + (kq ^ fx[e]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) step(kq + r, abase, r);
+    }
+    for (; kq < kc; ++kq) {
+      int abase[TM];
+#pragma unroll
+      for (int e = 0; e < TM; ++e) abase[e] = ra[e] + ((kq & ~3) ^ fx[e]);
+      step(kq, abase, kq & 3);
+    }
+  }
+  if (!active) return;
+  const int64_t c_m = p.coef[2][am], c_n = p.coef[2][an];
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t m = m0 + ra[i] / BK;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t n = n0 + rn[j];
+      if (n < N) C[m * c_m + n * c_n] = from_f32<In>(acc[i][j]);
+    }
+  }
+}
+
+// gemv: CTA = level-1 m tile, thread = TM rows (vthread slices), n ascending; x staged once in
+// shared memory when it fits; each row streamed with float4 loads (4 consecutive n, summed in
+// order), U loads per row in flight.
+template <int TM>
+__global__ void __launch_bounds__(256) k_simt_gemv(const GenericPlan p, const float* __restrict__ A,
+                                                   const float* __restrict__ x, float* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* xs = reinterpret_cast<float*>(smem_raw);
+  const int am = p.sp[0], an = p.red[0];
+  const int64_t M = p.ext[am], N = p.ext[an];
+  const int64_t b = blockIdx.y;
+  A += b * p.batch_stride[0];
+  x += b * p.batch_stride[1];
+  y += b * p.batch_stride[2];
+  const bool xin = p.fast_pad != 0;  // x staged
+  if (xin) {
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) xs[i] = x[i * p.coef[1][an]];
+    __syncthreads();
+  }
+  const int BM = p.B[0];
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+  if (static_cast<int>(threadIdx.x) >= p.slots) return;
+  const int per = TM / p.V[0], str = BM / p.V[0];
+  const float* row[TM];
+  bool ok[TM];
+  float acc[TM];
+#pragma unroll
+  for (int e = 0; e < TM; ++e) {
+    const int64_t m = m0 + (e / per) * str + static_cast<int>(threadIdx.x) * per + e % per;
+    ok[e] = m < M;
+    row[e] = A + (ok[e] ? m : 0) * p.coef[0][am];
+    acc[e] = 0.0f;
+  }
+  const int64_t a_n = p.coef[0][an];
+  const float* xv = xin ? xs : x;
+  const int64_t x_n = xin ? 1 : p.coef[1][an];
+  int64_t n = 0;
+  if (a_n == 1 && x_n == 1 && (p.coef[0][am] & 3) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    constexpr int U = TM <= 4 ? 4 : 2;  // float4 loads per row in flight
+    for (; n + 4 * U <= N; n += 4 * U) {
+      float4 v[TM][U];
+#pragma unroll
+      for (int e = 0; e < TM; ++e)
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[e][u] = __ldg(reinterpret_cast<const float4*>(row[e] + n) + u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 xx = *reinterpret_cast<const float4*>(xv + n + 4 * u);
+#pragma unroll
+        for (int e = 0; e < TM; ++e) {
+          acc[e] = fmaf(v[e][u].x, xx.x, acc[e]);
+          acc[e] = fmaf(v[e][u].y, xx.y, acc[e]);
+          acc[e] = fmaf(v[e][u].z, xx.z, acc[e]);
+          acc[e] = fmaf(v[e][u].w, xx.w, acc[e]);
+        }
+      }
+    }
+  }
+  for (; n < N; ++n) {
+    const float xx = xv[n * x_n];
+#pragma unroll
+    for (int e = 0; e < TM; ++e) acc[e] = fmaf(__ldg(row[e] + n * a_n), xx, acc[e]);
+  }
+#pragma unroll
+  for (int e = 0; e < TM; ++e) {
+    const int64_t m = m0 + (e / per) * str + static_cast<int>(threadIdx.x) * per + e % per;
+    if (ok[e]) y[m * p.coef[2][am]] = acc[e];
+  }
+}
+
+template <typename In>
+void launch_simt_gemm(const GenericPlan& p, const void* in0, const void* in1, void* out, int batch, cudaStream_t st) {
+  dim3 g(static_cast<unsigned>(p.tiles[0]) * static_cast<unsigned>(p.tiles[1]), static_cast<unsigned>(batch));
+  auto go = [&](auto kern) {
+    if (p.smem_bytes > 48 * 1024)
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes),
+                 "simt gemm smem attribute");
+    kern<<<g, p.block, p.smem_bytes, st>>>(p, static_cast<const In*>(in0), static_cast<const In*>(in1),
+                                          static_cast<In*>(out));
+    check_cuda(cudaGetLastError(), "simt gemm launch");
+    count_launch();
+  };
+  auto pick_n = [&](auto tm) {
+    constexpr int TM = decltype(tm)::value;
+    switch (p.T[1]) {
+      case 1: go(k_simt_gemm<In, TM, 1>); break;
+      case 2: go(k_simt_gemm<In, TM, 2>); break;
+      case 4: go(k_simt_gemm<In, TM, 4>); break;
+      case 8: go(k_simt_gemm<In, TM, 8>); break;
+      default: throw Error(Code::Unsupported, "simt gemm thread tile");
+    }
+  };
+  switch (p.T[0]) {
+    case 1: pick_n(std::integral_constant<int, 1>{}); break;
+    case 2: pick_n(std::integral_constant<int, 2>{}); break;
+    case 4: pick_n(std::integral_constant<int, 4>{}); break;
+    case 8: pick_n(std::integral_constant<int, 8>{}); break;
+    default: throw Error(Code::Unsupported, "simt gemm thread tile");
+  }
+}
+
+void launch_simt_gemv(const GenericPlan& p, const void* in0, const void* in1, void* out, int batch, cudaStream_t st) {
+  dim3 g(static_cast<unsigned>(p.tiles[0]), static_cast<unsigned>(batch));
+  auto go = [&](auto kern) {
+    if (p.smem_bytes > 48 * 1024)
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes),
+                 "simt gemv smem attribute");
+    kern<<<g, p.block, p.smem_bytes, st>>>(p, static_cast<const float*>(in0), static_cast<const float*>(in1),
+                                          static_cast<float*>(out));
+    check_cuda(cudaGetLastError(), "simt gemv launch");
+    count_launch();
+  };
+  switch (p.T[0]) {
+    case 1: go(k_simt_gemv<1>); break;
+    case 2: go(k_simt_gemv<2>); break;
+    case 4: go(k_simt_gemv<4>); break;
+    case 8: go(k_simt_gemv<8>); break;
+    default: throw Error(Code::Unsupported, "simt gemv thread tile");
+  }
+}
+
 template <typename In, typename Out, typename Acc>
 void dispatch(const GenericPlan& p, int width, const void* in0, const void* in1, void* out, int batch,
               cudaStream_t st) {
@@ -201,6 +478,17 @@ int generic_max_width(bool f64) { return f64 ? 16 : 32; }
 
 void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, const void* in1, void* out,
                     int batch, cudaStream_t st) {
+  if (!f64 && p.fast == 1) {
+    if (bf16)
+      launch_simt_gemm<__nv_bfloat16>(p, in0, in1, out, batch, st);
+    else
+      launch_simt_gemm<float>(p, in0, in1, out, batch, st);
+    return;
+  }
+  if (!f64 && !bf16 && p.fast == 2) {
+    launch_simt_gemv(p, in0, in1, out, batch, st);
+    return;
+  }
   const int width = p.acc / p.acc_chunks;
   if (bf16) {
     if (f64)

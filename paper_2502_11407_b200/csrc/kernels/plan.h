@@ -48,6 +48,10 @@ struct GenericPlan {
   int32_t divisor;             // avgpool: F*F (true window), 0 otherwise
   int32_t block;               // threads per CTA
   int32_t smem_bytes;
+  // register-tiled fast paths of the same plan (same tiles, vthreads and reduce order):
+  // 0 = the general walk, 1 = gemm (spatial m, n; reduce k), 2 = gemv (spatial m; reduce n)
+  int32_t fast;
+  int32_t fast_pad;            // gemm: row padding (floats) of the staged k-major A box
 };
 
 }  // namespace gb

@@ -215,3 +215,39 @@ def test_full_size_fp32_configs(name):
     # by sqrt(K / 64)
     k_red = 1024 if name == "G" else 64 * 9
     assert err <= F32_TOL * np.sqrt(k_red / 64), err
+
+
+FAST = [
+    ("gemm", {"kind": "gemm", "M": 1024, "K": 1024, "N": 1024}),   # G: 16 B asynchronous copies
+    ("gemm", {"kind": "gemm", "M": 200, "K": 97, "N": 136}),       # ragged tiles, 4 B copies (K % 4 != 0)
+    ("gemm", {"kind": "gemm", "M": 96, "K": 64, "N": 80, "dtype_bytes": 2, "batch": 3}),  # bf16, batched
+    ("gemv", {"kind": "gemv", "M": 32768, "N": 4096}),            # V
+    ("gemv", {"kind": "gemv", "M": 1000, "N": 999}),              # ragged, scalar tail
+]
+
+
+@pytest.mark.parametrize("kind,doc", FAST, ids=lambda x: json.dumps(x) if isinstance(x, dict) else x)
+def test_simt_fast_paths_match_the_general_walk(kind, doc):
+    """simt_f32's register-tiled gemm / gemv kernels run the SAME plan (tiles, vthreads, ascending
+    single-axis reduce) as the general walk: the plan says which path ran, outputs are bit-exact on
+    integer inputs and within the fp32 bar on U(-1,1) against the oracle's interpret(); for every
+    top-k state (different tiles / vthreads)."""
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    sched = g.optimize(op, g.HardwareSpec.b200(0), g.EngineConfig(seed=0, mode="b200", top_k=3))
+    rng = np.random.default_rng(5)
+    bf16 = op.dtype_bytes == 2
+    for idx in range(len(sched)):
+        k = g.Kernel(op, sched, idx, "simt_f32")
+        if k.info["plan"].get("fast") == "none":
+            continue
+        assert k.info["plan"]["fast"] == kind
+        for integer in (True, False):
+            _, xs = _inputs(doc, rng, integer)
+            ref = O.interpret(doc, sched[idx]["state"], xs, threads=os.cpu_count() or 8)
+            got = _run(op, sched, idx, "simt_f32", xs, ref.size)
+            if integer:
+                assert np.array_equal(got, _round(ref, bf16)), (idx, np.abs(got - ref).max())
+            else:
+                k_red = doc["K"] if kind == "gemm" else doc["N"]
+                tol = (1e-2 if bf16 else F32_TOL * max(1.0, np.sqrt(k_red / 64)))
+                assert np.abs(got - ref).max() / np.abs(ref).max() <= tol, idx
