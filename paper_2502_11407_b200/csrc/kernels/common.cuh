@@ -24,6 +24,14 @@ inline const char* dev_env(const char* name) {
 }
 void count_launch(uint64_t n = 1);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (cached): setting it
+// on every launch put host-side attribute work between dependent launches
+void set_smem_attr(const void* kern, size_t bytes, const char* what);
+template <typename F>
+inline void set_smem_attr(F* kern, size_t bytes, const char* what) {
+  set_smem_attr(reinterpret_cast<const void*>(kern), bytes, what);
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f32(T v);
 template <>

@@ -286,8 +286,7 @@ void run_gemm_conv(const ConvGemmArgs& a, const CUtensorMap& mapW, const float* 
   count_launch();
   auto kern = k_conv_gemm<BN, STAGES>;
   const size_t smem = STAGES * STAGE + 16384 + 1024 + 256;
-  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-             "conv_gemm smem attribute");
+  set_smem_attr(kern, static_cast<int>(smem), "conv_gemm smem attribute");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGThreads);

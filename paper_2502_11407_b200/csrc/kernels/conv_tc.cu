@@ -415,16 +415,13 @@ void run_conv(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const fl
   T* ws_x = reinterpret_cast<T*>(static_cast<char*>(ws) + a.x_off);
   auto launch = [&](auto kern) {
     const size_t smem = g.w_bytes + static_cast<size_t>(g.stages) * g.a_bytes + 1024 + 256;
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "conv_tc smem attribute");
+    set_smem_attr(kern, static_cast<int>(smem), "conv_tc smem attribute");
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * a.C * a.R * a.S;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
     const int band = kPrepassBand;
     const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
-    check_cuda(cudaFuncSetAttribute(k_conv_prepass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(pre_smem)),
-               "prepass smem attribute");
+    set_smem_attr(k_conv_prepass<T>, static_cast<int>(pre_smem), "prepass smem attribute");
     k_conv_prepass<T><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(I, K, ws_x, ws_w, a.N, a.C,
                                                                                          a.H, a.W, a.F, a.R * a.S, band);
     check_cuda(cudaGetLastError(), "conv prepass launch");
@@ -828,8 +825,7 @@ void run_conv_ns(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const
   float* ws_x = reinterpret_cast<float*>(static_cast<char*>(ws) + a.x_off);
   auto launch = [&](auto kern) {
     const size_t smem = g.w_bytes + static_cast<size_t>(g.stages) * g.a_bytes + 1024 + g.stage_o + 1024;
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "conv_ns smem attribute");
+    set_smem_attr(kern, static_cast<int>(smem), "conv_ns smem attribute");
     mk.mark(st);
     const int64_t wt = static_cast<int64_t>(a.F) * g.gC * g.gR * g.gS;
     const int wblocks = static_cast<int>(std::min<int64_t>(64, (wt + 255) / 256));
@@ -839,16 +835,13 @@ void run_conv_ns(const ConvTcArgs& a, const ConvTcMaps& m, const float* I, const
     } else if (a.s2d) {
       const int xblocks = static_cast<int>(std::min<int64_t>(1 << 20, static_cast<int64_t>(a.N) * g.gH));  // a row per block
       const size_t rsm = static_cast<size_t>(a.C) * 2 * a.W * sizeof(float);
-      check_cuda(cudaFuncSetAttribute(k_s2d_prepass, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm)),
-                 "s2d smem attribute");
+      set_smem_attr(k_s2d_prepass, static_cast<int>(rsm), "s2d smem attribute");
       k_s2d_prepass<<<xblocks + wblocks, 256, rsm, st>>>(I, K, ws_x, ws_w, a.N, a.C, a.H, a.W, a.F, a.R, a.S, g.gH,
                                                        g.gW, g.gR, g.gS, xblocks);
     } else {
       const int band = kPrepassBand;
       const size_t pre_smem = static_cast<size_t>(a.C) * (band * a.W + 1) * sizeof(float);
-      check_cuda(cudaFuncSetAttribute(k_conv_prepass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(pre_smem)),
-                 "prepass smem attribute");
+      set_smem_attr(k_conv_prepass<float>, static_cast<int>(pre_smem), "prepass smem attribute");
       k_conv_prepass<float><<<a.N * ((a.H + band - 1) / band) + wblocks, 256, pre_smem, st>>>(
           I, K, ws_x, ws_w, a.N, a.C, a.H, a.W, a.F, a.R * a.S, band);
     }

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -32,6 +33,16 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_smem_attr(const void* kern, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[kern];
+  if (have >= bytes) return;
+  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)), what);
+  have = bytes;
+}
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 
@@ -466,6 +477,8 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           }
           pi << "],\"tiles\":" << c.total << ",\"grid\":" << std::min(c.total, sms) << ",\"stages\":" << c.stages
              << ",\"mma_issue\":\"" << (c.spec >= 0 ? "specialised (3x3, W mod 4)" : "table-driven")
+             << "\",\"cta_pair\":" << (c.pair ? "true" : "false") << ",\"prezero\":" << c.tb.prezero
+             << ",\"grid_note\":\"" << (c.pair ? "clusters of 2 CTAs, UMMA M = 256 (cta_group::2), half the bank per CTA" : "one CTA per tile stream")
              << "\",\"block\":576,\"launches\":2,\"A\":\"MN-major TMA boxes straight from the NCHW input\",\"B\":\"bank image converted by a PDL-chained launch, bulk-copied, resident\"}";
         } else if (op.kind == Kind::Conv2d && conv_tc_ok(op, bf16) &&
                    !(dev_env("GENSOR_CONV_FAMILY") && std::string(dev_env("GENSOR_CONV_FAMILY")) == "gemm" &&
@@ -654,7 +667,8 @@ void* stream_workspace(const Kernel* k, cudaStream_t st) {
   cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
   check_cuda(cudaThreadExchangeStreamCaptureMode(&mode), "capture mode");
   void* p = nullptr;
-  const cudaError_t e = cudaMalloc(&p, k->ws_bytes);
+  cudaError_t e = cudaMalloc(&p, k->ws_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, k->ws_bytes);  // families keep completion counters in it
   cudaThreadExchangeStreamCaptureMode(&mode);
   check_cuda(e, "kernel workspace");
   k->ws_slots.push_back({st, p});
@@ -712,6 +726,7 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
   for (int i = 0; i < n_in; ++i)
     if (!d_in[i]) throw Error(Code::ShapeMismatch, "null input pointer");
   auto st = static_cast<cudaStream_t>(stream);
+  const bool own_ws = !ws;
   if (k->ws_bytes) {
     if (!ws)
       ws = stream_workspace(k, st);
@@ -751,7 +766,7 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
     case Family::ConvFlat: {
       CallMaps m;
       call_maps(k, d_in, n_in, d_out, ws, m);
-      launch_conv_flat(k->flat, m.x, d_in[1], d_out, ws, st, mk);
+      launch_conv_flat(k->flat, m.x, d_in[1], d_out, ws, own_ws, st, mk);
       break;
     }
     case Family::Stream:

@@ -29,10 +29,22 @@ struct FlatTable {
   int op_n[kFlatMaxOps] = {};                    // UMMA N (taps * FN)
   int op_brow[kFlatMaxOps] = {};                 // first filter row inside a chunk of the bank
   int op_zero[kFlatMaxOps] = {};                 // first touch: zero-initialise at k-step 0
+  // pair mode (cta_group::2: each CTA of the pair holds half of every run's filter rows): runs are
+  // never split — blocks a run would only partly find written are zeroed ahead (prezero) by the
+  // epilogue, so every run is one op in both passes and its half-rows sit at one bank offset
+  bool pair = false;
+  uint32_t prezero = 0;                          // accumulator blocks zeroed before each tile
+  int nruns = 0;
+  int run_rows[kFlatMaxTaps] = {};               // N = taps * FN
+  int run_hbase[kFlatMaxTaps] = {};              // first row of the run's half in a CTA's bank chunk
+  int tap_run[kFlatMaxTaps] = {};                // run of tap t
+  int tap_rrow[kFlatMaxTaps] = {};               // first row of tap t inside its run (slot offset * FN)
+  int half_rows = 0;                             // rows of one CTA's bank chunk (sum of N / 2)
 };
 
-constexpr FlatTable flat_table(int R, int S, int W, int FN) {
+constexpr FlatTable flat_table(int R, int S, int W, int FN, bool pair = false) {
   FlatTable tb{};
+  tb.pair = pair;
   const int T = R * S;
   if (T < 1 || T > kFlatMaxTaps || FN < 16 || FN > 64 || FN % 16) return tb;
   int run_b0[kFlatMaxTaps] = {}, run_cnt[kFlatMaxTaps] = {}, run_slot0[kFlatMaxTaps] = {};
@@ -57,6 +69,8 @@ constexpr FlatTable flat_table(int R, int S, int W, int FN) {
         ++group_nrun[g];
       }
       ++run_cnt[nruns - 1];
+      tb.tap_run[t] = nruns - 1;
+      tb.tap_rrow[t] = (slot - run_slot0[nruns - 1]) * FN;
       tb.tap_slot[t] = slot++;
       tb.bmask |= 1u << b;
       prev_b = b;
@@ -65,6 +79,12 @@ constexpr FlatTable flat_table(int R, int S, int W, int FN) {
   }
   for (int ri = 0; ri < nruns; ++ri)
     if (run_cnt[ri] * FN > 256) return tb;  // UMMA N <= 256
+  tb.nruns = nruns;
+  for (int ri = 0; ri < nruns; ++ri) {
+    tb.run_rows[ri] = run_cnt[ri] * FN;
+    tb.run_hbase[ri] = tb.half_rows;
+    tb.half_rows += run_cnt[ri] * FN / 2;
+  }
   int nops = 0;
   for (int pass = 0; pass < 2; ++pass) {
     uint32_t written = 0;
@@ -72,6 +92,10 @@ constexpr FlatTable flat_table(int R, int S, int W, int FN) {
       tb.grp_op0[pass][g] = nops;
       for (int ri = group_run0[g]; ri < group_run0[g] + group_nrun[g]; ++ri) {
         const uint32_t mask = ((1u << run_cnt[ri]) - 1u) << run_b0[ri];
+        if (pair && pass == 0 && (written & mask) != 0 && (written & mask) != mask) {
+          tb.prezero |= mask & ~written;  // zeroed ahead: the run accumulates into all its blocks
+          written |= mask;
+        }
         const bool whole = pass == 1 || (written & mask) == mask || (written & mask) == 0;
         const int pieces = whole ? 1 : run_cnt[ri];
         for (int jb = 0; jb < pieces; ++jb) {
@@ -81,7 +105,7 @@ constexpr FlatTable flat_table(int R, int S, int W, int FN) {
           const uint32_t bits = ((1u << cnt) - 1u) << b0;
           tb.op_dcol[nops] = b0 * FN;
           tb.op_n[nops] = cnt * FN;
-          tb.op_brow[nops] = (run_slot0[ri] + (whole ? 0 : jb)) * FN;
+          tb.op_brow[nops] = pair ? tb.run_hbase[ri] : (run_slot0[ri] + (whole ? 0 : jb)) * FN;
           tb.op_zero[nops] = pass == 0 && (written & bits) == 0 ? 1 : 0;
           ++nops;
         }

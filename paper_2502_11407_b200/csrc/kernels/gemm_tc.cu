@@ -450,8 +450,7 @@ template <int STAGES>
 void run_x3(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   const size_t smem = STAGES * 2 * (128 * 128 + 64 * 128) + 4 * 32 * 64 * 4 + 1024 + 256;
   auto kern = k_gemm_x3<STAGES>;
-  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-             "gemm_x3 smem attribute");
+  set_smem_attr(kern, static_cast<int>(smem), "gemm_x3 smem attribute");
   const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + 63) / 64;
   const int total = tiles_m * tiles_n * a.batch;
   const int dbg = dev_env("GENSOR_X3_DBG") ? std::atoi(dev_env("GENSOR_X3_DBG")) : 0;
@@ -465,8 +464,7 @@ void run_cs(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   constexpr uint32_t STAGE = 128 * 128 + BN * 128;
   const size_t smem = STAGES * STAGE + SB * 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
   auto kern = k_gemm_tc<T, TOut, BN, STAGES, CS, SB>;
-  check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-             "gemm_tc smem attribute");
+  set_smem_attr(kern, static_cast<int>(smem), "gemm_tc smem attribute");
   const int tiles_m = (a.M + 127) / 128, tiles_n = (a.N + BN - 1) / BN;
   const int total = tiles_m * tiles_n * a.batch;
   if constexpr (CS == 1) {

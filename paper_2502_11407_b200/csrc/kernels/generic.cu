@@ -400,8 +400,7 @@ void launch_simt_gemm(const GenericPlan& p, const void* in0, const void* in1, vo
   dim3 g(static_cast<unsigned>(p.tiles[0]) * static_cast<unsigned>(p.tiles[1]), static_cast<unsigned>(batch));
   auto go = [&](auto kern) {
     if (p.smem_bytes > 48 * 1024)
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes),
-                 "simt gemm smem attribute");
+      set_smem_attr(kern, p.smem_bytes, "simt gemm smem attribute");
     kern<<<g, p.block, p.smem_bytes, st>>>(p, static_cast<const In*>(in0), static_cast<const In*>(in1),
                                           static_cast<In*>(out));
     check_cuda(cudaGetLastError(), "simt gemm launch");
@@ -430,8 +429,7 @@ void launch_simt_gemv(const GenericPlan& p, const void* in0, const void* in1, vo
   dim3 g(static_cast<unsigned>(p.tiles[0]), static_cast<unsigned>(batch));
   auto go = [&](auto kern) {
     if (p.smem_bytes > 48 * 1024)
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes),
-                 "simt gemv smem attribute");
+      set_smem_attr(kern, p.smem_bytes, "simt gemv smem attribute");
     kern<<<g, p.block, p.smem_bytes, st>>>(p, static_cast<const float*>(in0), static_cast<const float*>(in1),
                                           static_cast<float*>(out));
     check_cuda(cudaGetLastError(), "simt gemv launch");
@@ -454,8 +452,7 @@ void dispatch(const GenericPlan& p, int width, const void* in0, const void* in1,
   dim3 g(static_cast<unsigned>(grid), static_cast<unsigned>(batch));
   auto go = [&](auto kern) {
     if (p.smem_bytes > 48 * 1024)
-      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes),
-                 "generic smem attribute");
+      set_smem_attr(kern, p.smem_bytes, "generic smem attribute");
     kern<<<g, p.block, p.smem_bytes, st>>>(p, static_cast<const In*>(in0), static_cast<const In*>(in1),
                                           static_cast<Out*>(out));
     check_cuda(cudaGetLastError(), "generic launch");

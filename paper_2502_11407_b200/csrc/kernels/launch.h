@@ -99,14 +99,17 @@ struct ConvFlatArgs {
   int PW = 0;    // wide positions per image (OH * W)
   int tiles_img = 0, total = 0, stages = 0, sms = 148;
   int spec = -1; // compile-time-specialised MMA issue (3x3, FN 64: W mod 4), -1 = table-driven
+  bool pair = false;  // cta_group::2 CTA pairs (flat_table pair mode: half the bank per CTA)
   int exp = 0;   // developer experiments (DEV build, GENSOR_FLAT_EXP): 0 in the product
-  size_t ws_bytes = 0;  // bank image W' (workspace), rewritten by every execute
+  size_t ws_bytes = 0;  // bank image W' (workspace), rewritten by every execute, + completion counter
+  size_t sync_off = 0;  // counter of filter CTAs done (handle-owned workspaces)
+  int filt_blocks = 0;  // CTAs of the bank-conversion launch
   FlatTable tb;         // taps, groups and the MMA op table for this W (flat_table.h)
 };
 bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a);
 void conv_flat_map(const ConvFlatArgs& a, const void* I, CUtensorMap& mapX);
 void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void* K, void* O, void* ws,
-                      cudaStream_t st, Marks& mk);
+                      bool own_ws, cudaStream_t st, Marks& mk);
 
 // ---- HBM-streaming family (stream.cu): gemv / softmax / avgpool2d / dwconv2d ----
 enum class StreamKind : int { Gemv, Softmax, AvgPool, DwConv };

@@ -742,8 +742,7 @@ void run_window(const StreamWinArgs& a, const void* in, const void* w, void* out
   if (a.vec) {  // 16 B aligned input: TMA bulk band loads
     auto kern = k_window_bulk<DW, MODE>;
     const size_t smem = kWinBulkStages * (a.buf_floats * sizeof(float) + 16);
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "window smem attribute");
+    set_smem_attr(kern, static_cast<int>(smem), "window smem attribute");
     const int threads = a.threads + 32;
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "window occupancy");
     const int64_t grid = std::min<int64_t>(a.units, static_cast<int64_t>(std::max(1, per_sm)) * a.sms);
@@ -753,8 +752,7 @@ void run_window(const StreamWinArgs& a, const void* in, const void* w, void* out
   } else {  // 4 B aligned input: per-thread cp.async staging
     auto kern = k_window<DW, MODE>;
     const size_t smem = kWinStages * a.buf_floats * sizeof(float);
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "window smem attribute");
+    set_smem_attr(kern, static_cast<int>(smem), "window smem attribute");
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, a.threads, smem), "window occupancy");
     const int64_t grid = std::min<int64_t>(a.units, static_cast<int64_t>(std::max(1, per_sm)) * a.sms);
     kern<<<static_cast<unsigned>(grid), a.threads, smem, st>>>(a, static_cast<const float*>(in),
@@ -794,8 +792,7 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
       stages = stages / kGemvBulkConsumers * kGemvBulkConsumers;
       if (vec && a.N >= 256 && stages >= kGemvBulkConsumers) {
         const size_t smem = row_bytes * (stages + 1) + static_cast<size_t>(stages) * 16 + 16;
-        check_cuda(cudaFuncSetAttribute(k_gemv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-                   "gemv smem attribute");
+        set_smem_attr(k_gemv_bulk, static_cast<int>(smem), "gemv smem attribute");
         const int64_t grid = std::min<int64_t>(units, a.sms);
         k_gemv_bulk<<<static_cast<unsigned>(grid), 32 * (kGemvBulkConsumers + 1), smem, st>>>(
             static_cast<const float*>(in0), static_cast<const float*>(in1), static_cast<float*>(out), a.M, a.N,
@@ -843,8 +840,7 @@ void launch_stream(const StreamArgs& a, const void* in0, const void* in1, void* 
         const int64_t groups = (w.planes + kGlobalPlanes - 1) / kGlobalPlanes;
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, static_cast<int64_t>(w.sms) * 4));
         auto kern = dw ? k_window_global<true> : k_window_global<false>;
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-                   "global window smem attribute");
+        set_smem_attr(kern, static_cast<int>(smem), "global window smem attribute");
         kern<<<grid, kGlobalPlanes, smem, st>>>(w, static_cast<const float*>(in0), static_cast<const float*>(in1),
                                                 static_cast<float*>(out));
         check_cuda(cudaGetLastError(), "global window launch");

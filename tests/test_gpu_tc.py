@@ -121,6 +121,10 @@ CONVS = [
     {"kind": "conv2d", "I": [2, 32, 30, 30], "K": [64, 32, 3, 3], "S": 1},    # 7 tiles per image
     {"kind": "conv2d", "I": [1, 32, 20, 24], "K": [32, 32, 5, 5], "S": 1},    # 25 taps, runs of 4
     {"kind": "conv2d", "I": [1, 96, 10, 10], "K": [16, 96, 3, 3], "S": 1},    # 3 chunks, FN = 16
+    # conv_flat CTA pairs (3x3, FN = 64): the four W mod 4 classes, an odd tile count
+    {"kind": "conv2d", "I": [2, 32, 12, 13], "K": [64, 32, 3, 3], "S": 1},    # W = 1 (mod 4)
+    {"kind": "conv2d", "I": [2, 64, 12, 15], "K": [64, 64, 3, 3], "S": 1},    # W = 3 (mod 4)
+    {"kind": "conv2d", "I": [3, 32, 8, 12], "K": [64, 32, 3, 3], "S": 1},     # 3 tiles: the pair's last tile recomputed
 ]
 
 

@@ -58,13 +58,16 @@ fn.argtypes = [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 buf = (ctypes.c_longlong * (160 * 64))()
 flush.zero_()
 torch.cuda.synchronize()
+torch.cuda._sleep(200_000)  # as the bench: the host enqueues while the device is busy
 k.execute(xs, out)
 torch.cuda.synchronize()
 assert fn(buf, 160 * 64) == 0
 tr = np.array(buf, dtype=np.int64).reshape(160, 64)[:148]
+if k.info["plan"].get("cta_pair"):
+    tr = tr[0::2]  # pair leaders carry the MMA marks
 rel = tr - tr[:, :1]
 rows = []
-for c in range(148):
+for c in range(len(tr)):
     r = rel[c]
     nt = sum(1 for i in range(6) if tr[c, 16 + i] != 0)
     rows.append((c, nt, r[1], r[2], [r[8 + i] for i in range(nt)], [r[16 + i] for i in range(nt)],
@@ -74,6 +77,28 @@ for row in rows[:6] + rows[-2:]:
 end = np.array([r[-1] for r in rows])
 print("end clk: median", np.median(end), "max", end.max(), "min", end.min())
 first_mma = np.array([r[4][0] for r in rows])
+fl = lib.gensor_dev_flat_filt
+fl.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+fb = (ctypes.c_ulonglong * 5)()
+fl(fb)
+flush.zero_()
+torch.cuda.synchronize()
+torch.cuda._sleep(200_000)  # the host enqueues while the device is busy: device-side gaps only
+a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a0.record()
+k.execute(xs, out)
+b0.record()
+b0.synchronize()
+fl(fb)
+assert fn(buf, 160 * 64) == 0
+tg = np.array(buf, dtype=np.int64).reshape(160, 64)[:148]
+print("globaltimer (ns): filters start..end", int(fb[1] - fb[0]), "| conv CTAs first start - filters start", int(tg[:, 50].min() - fb[0]),
+      "| conv CTA start spread", int(tg[:, 50].max() - tg[:, 50].min()), "| conv span (first start .. last end)", int(tg[:, 51].max() - tg[:, 50].min()),
+      "| filters start .. conv end", int(tg[:, 51].max() - fb[0]), "| events", a0.elapsed_time(b0) * 1e3)
+print("filters start -> last counter increment", int(fb[3] - fb[0]) if fb[3] else None, "| -> first conv observation", int(fb[4] - fb[0]) if fb[4] < 2**63 else None)
+if fb[2]:
+    print("marker -> filters start", int(fb[0] - fb[2]), "| marker -> conv first CTA", int(tg[:, 50].min() - fb[2]), "| marker -> conv end", int(tg[:, 51].max() - fb[2]))
+print("pair start marks (alloc, prezero(w2), cluster sync, griddep):", np.median(rel[:, 2]), np.median(tr[:, 5] - tr[:, 0]), np.median(rel[:, 3]), np.median(rel[:, 4]))
 print("first MMA start: median", np.median(first_mma), "griddep wait", np.median([r[2] for r in rows]),
       "filters ready", np.median([r[3] for r in rows]))
 mma = [r[5][i] - r[4][i] for r in rows for i in range(r[1])]
