@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     // (the input does not depend on the filter launch: no griddepcontrol.wait here)
     if (elect_one()) {
       tma_prefetch(&mapX);
-      if (a.exp & 131072) mbar_wait(&bank_bar[0], 0);  // DEV: input stages only after the bank image
       int it = 0;
       for (int t = blockIdx.x; t < a.total; t += gridDim.x) {
         const int n = t / a.tiles_img;
@@ -294,10 +293,6 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
           for (int g = 0; g < tb.ngroups; ++g, ++it) {
             const int st = it % STAGES;
             mbar_wait_sleep(&empty[st], ((it / STAGES) & 1) ^ 1);
-            if ((a.exp & 4) && it >= STAGES) {  // DEV experiment: no TMA after the first ring (timing only)
-              mbar_arrive(&full[st]);
-              continue;
-            }
             mbar_arrive_expect_tx(&full[st], kFlatStage);
             uint8_t* dst = ring + st * kFlatStage;
             const int x0 = p0 + (tb.group_o[g] & ~3);
@@ -392,12 +387,6 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       if (warp == 2 && lane == 0 && local < 6) FL_MARK(24 + local);
       tc_fence_after();
-      if (a.exp & 32) {  // DEV experiment: epilogue does nothing but release (timing only)
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[acc]);
-        continue;
-      }
       uint32_t r[kFlatNfbh][4][16];
 #pragma unroll
       for (int x = 0; x < kFlatNfbh; ++x) {
@@ -457,7 +446,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         }
       }
       if (warp == 2 && lane == 0 && local == 1) FL_MARK(46);
-      if (!(a.exp & 64)) named_bar(1 + h, 128);  // DEV 64: no exchange barrier (timing only)
+      named_bar(1 + h, 128);
       if (warp == 2 && lane == 0 && local == 1) FL_MARK(47);
       if (lane < 3 && q < 3) {
 #pragma unroll
@@ -685,7 +674,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     }
     tmem_st_wait();
   };
-  if (nmine && tb.prezero && !(a.exp & 16384)) {  // DEV 16384: skip (timing only)
+  if (nmine && tb.prezero) {
     prezero(0);
     prezero(1);
   }
@@ -700,7 +689,6 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     // ---- producer (each CTA): its tile's stages; completion counted on the leader's full barrier
     if (elect_one()) {
       tma_prefetch(&mapX);
-      if (a.exp & 131072) mbar_wait(&bank_bar[0], 0);  // DEV: input stages only after the bank image
       int it = 0;
       for (int tp = pair; tp < pairs_total; tp += npairs) {
         int t = 2 * tp + static_cast<int>(rank);
@@ -1001,9 +989,7 @@ void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void
     }();
     (void)carve;
   }
-  if (a.exp & 4096) {
-    // DEV 4096: keep the previous execute's bank image (timing only)
-  } else if (a.pair)
+  if (a.pair)
     k_flat_filters_pair<<<a.filt_blocks, 128, 0, st>>>(static_cast<const float*>(K), static_cast<uint8_t*>(ws), a, sync);
   else
     k_flat_filters<<<a.filt_blocks, 128, 0, st>>>(static_cast<const float*>(K), static_cast<uint8_t*>(ws), a, sync);
@@ -1026,10 +1012,6 @@ void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.pair ? 2 : 1;
-    if (a.exp & 32768) {  // DEV 32768: no programmatic dependent launch (timing only)
-      cfg.attrs = attr + 1;
-      cfg.numAttrs = a.pair ? 1 : 0;
-    }
     check_cuda(cudaLaunchKernelEx(&cfg, kern, mapX, a, static_cast<const uint8_t*>(ws), static_cast<float*>(O), sync),
                "conv_flat launch");
     count_launch();

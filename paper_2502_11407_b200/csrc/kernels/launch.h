@@ -100,7 +100,7 @@ struct ConvFlatArgs {
   int tiles_img = 0, total = 0, stages = 0, sms = 148;
   int spec = -1; // compile-time-specialised MMA issue (3x3, FN 64: W mod 4), -1 = table-driven
   bool pair = false;  // cta_group::2 CTA pairs (flat_table pair mode: half the bank per CTA)
-  int exp = 0;   // developer experiments (DEV build, GENSOR_FLAT_EXP): 0 in the product
+  int exp = 0;   // DEV build only (GENSOR_FLAT_EXP): 2048 table-driven issue, 8192 single CTAs, 65536 timeline marker
   size_t ws_bytes = 0;  // bank image W' (workspace), rewritten by every execute, + completion counter
   size_t sync_off = 0;  // counter of filter CTAs done (handle-owned workspaces)
   int filt_blocks = 0;  // CTAs of the bank-conversion launch
