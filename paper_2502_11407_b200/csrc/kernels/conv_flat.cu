@@ -653,16 +653,18 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     mbar_init(peer_bar, 1);
     fence_barrier_init();
   }
+  cluster_sync();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA completion
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) FL_MARK(2);
   const uint32_t tmem = *tmem_slot;
-  // blocks a run only partly finds written start the tile at zero: both accumulator buffers now,
-  // then each buffer again right after the epilogue has read it
   const int q = warp & 3, h = (warp - 2) >> 2;
   const int nmine = warp >= 2 && h < nfb ? (nfb - h + EPW - 1) / EPW : 0;
+  // blocks a run only partly finds written start each tile at zero (the epilogue re-zeroes a
+  // buffer right after reading it); the first zeroing of both buffers is the epilogue warps'
+  // initial release of the accumulators, so nothing waits on it before the first MMA
   auto prezero = [&](int acc) {
     uint32_t z[16];
 #pragma unroll
@@ -674,15 +676,14 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     }
     tmem_st_wait();
   };
-  if (nmine && tb.prezero) {
-    prezero(0);
-    prezero(1);
-  }
-  if (threadIdx.x == 64) FL_MARK(5);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();  // barriers initialised and accumulators zeroed in both CTAs before any cross-CTA traffic
-  tc_fence_after();
+  auto release = [&](int acc) {  // this warp is done with accumulator buffer acc
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (leader) mbar_arrive(&acc_empty[acc]);
+      else mbar_arrive_remote(&acc_empty[acc], 0);
+    }
+  };
   if (threadIdx.x == 0) FL_MARK(3);
 
   if (warp == 0) {
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         c.local = 0;
         for (int tp = pair; tp < pairs_total; tp += npairs, ++c.local) {
           const int acc = c.local & 1;
-          mbar_wait(&acc_empty[acc], ((c.local >> 1) & 1) ^ 1);
+          mbar_wait(&acc_empty[acc], (c.local >> 1) & 1);  // phase 0 = the epilogue's initial release
           if (c.local < 6) FL_MARK(8 + c.local);
           tc_fence_after();
           c.d = tmem + acc * 256;
@@ -761,6 +762,12 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     const int nloop = nmine ? pairs_total : 0;
     const int plane_out = a.OH * a.OW;
     const uint32_t bm = tb.bmask;
+    if (nmine) {
+      for (int acc = 0; acc < 2; ++acc) {
+        if (tb.prezero) prezero(acc);
+        release(acc);
+      }
+    }
     int local = 0;
     for (int tp = pair; tp < nloop; tp += npairs, ++local) {
       const int acc = local & 1;
@@ -795,12 +802,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
 #pragma unroll
         for (int b = 0; b < 4; ++b) tmem_ld_pin(r[x][b]);
       if (tb.prezero) prezero(acc);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {  // (no data is published: the TMEM reads are complete, a plain arrive suffices)
-        if (leader) mbar_arrive(&acc_empty[acc]);
-        else mbar_arrive_remote(&acc_empty[acc], 0);
-      }
+      release(acc);  // (no data is published: the TMEM reads are complete, a plain arrive suffices)
       if (bm != 15u) {
 #pragma unroll
         for (int x = 0; x < kFlatNfbh; ++x)
