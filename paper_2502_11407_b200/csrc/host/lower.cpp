@@ -163,7 +163,7 @@ std::string plan_json(const GenericPlan& p) {
      << ",\"acc\":" << p.acc << ",\"acc_chunks\":" << p.acc_chunks << ",\"rounds\":" << p.rounds
      << ",\"n_chunks\":" << p.n_chunks << ",\"chunk_len\":" << p.chunk_len << ",\"staged\":" << p.staged
      << ",\"smem_bytes\":" << p.smem_bytes
-     << ",\"fast\":\"" << (p.fast == 1 ? "gemm" : p.fast == 2 ? "gemv" : "none") << "\",\"block_tile\":[";
+     << ",\"fast\":\"" << (p.fast == 1 ? "gemm" : p.fast == 2 ? "gemv" : p.fast == 3 ? "gemv_tma" : "none") << "\",\"block_tile\":[";
   for (int i = 0; i < p.nsp; ++i) os << (i ? "," : "") << p.B[i];
   os << "],\"thread_tile\":[";
   for (int i = 0; i < p.nsp; ++i) os << (i ? "," : "") << p.T[i];

@@ -58,7 +58,7 @@ struct CallMaps {
   GemmTcMaps g;
   ConvTcMaps c;
   CUtensorMap w;
-  CUtensorMap x;  // conv_flat: the caller's NCHW input as {H*W, N*C}
+  CUtensorMap x;  // conv_flat: the caller's NCHW input as {H*W, N*C}; simt gemv (fast 3): A as {N, M}
 };
 constexpr int kMapCache = 4;
 
@@ -351,6 +351,15 @@ void simt_fast_path(const OpDesc& op, GenericPlan& p, int64_t optin) {
     p.smem_bytes = static_cast<int32_t>(smem);
   } else if (op.kind == Kind::Gemv && p.nsp == 1 && tile_ok(p.T[0]) && op.dtype_bytes == 4) {
     const int64_t n = p.ext[p.red[0]];
+    // TMA path: every thread owns one row per row group (vthreads == thread tile), unit-stride
+    // 16 B-aligned rows, at most 256 threads, x resident in shared memory
+    const int64_t tma_smem = 1024 + 3LL * p.slots * 128 * 8 + n * 4;
+    if (p.V[0] == p.T[0] && p.coef[0][p.red[0]] == 1 && (p.coef[0][p.sp[0]] & 3) == 0 && p.slots <= 256 &&
+        p.slots % 8 == 0 && op.batch == 1 && tma_smem <= optin) {
+      p.fast = 3;
+      p.smem_bytes = static_cast<int32_t>(tma_smem);
+      return;
+    }
     p.fast = 2;
     p.fast_pad = n * 4 <= std::min<int64_t>(optin, 96 * 1024) ? 1 : 0;  // x staged in shared memory
     p.smem_bytes = p.fast_pad ? static_cast<int32_t>(n * 4) : 0;
@@ -706,6 +715,15 @@ void call_maps(const Kernel* k, const void* const* d_in, int n_in, void* d_out, 
     case Family::ConvFlat:
       conv_flat_map(k->flat, d_in[0], fresh.x);
       break;
+    case Family::Generic:
+      if (k->gplan.fast == 3) {  // simt gemv through TMA: A[M][N] row-major, box {32 columns, slots rows}
+        const GenericPlan& p = k->gplan;
+        const uint64_t dims[2] = {static_cast<uint64_t>(p.ext[p.red[0]]), static_cast<uint64_t>(p.ext[p.sp[0]])};
+        const uint64_t strides[1] = {static_cast<uint64_t>(p.coef[0][p.sp[0]]) * 4};
+        const uint32_t box[2] = {32, static_cast<uint32_t>(p.slots)};
+        encode_map(&fresh.x, false, false, d_in[0], 2, dims, strides, box);
+      }
+      break;
     default:
       break;
   }
@@ -737,12 +755,19 @@ void execute(const Kernel* k, const void* const* d_in, int n_in, void* d_out, vo
   Marks mk;
   if (k->timing) mk.ev = k->ev;
   switch (k->family) {
-    case Family::Generic:
+    case Family::Generic: {
+      const CUtensorMap* gm = nullptr;
+      CallMaps m;
+      if (k->gplan.fast == 3) {
+        call_maps(k, d_in, n_in, d_out, ws, m);
+        gm = &m.x;
+      }
       mk.mark(st);
       launch_generic(k->gplan, k->f64, op.dtype_bytes == 2, d_in[0], n_in > 1 ? d_in[1] : nullptr, d_out,
-                     static_cast<int>(op.batch), st);
+                     static_cast<int>(op.batch), st, gm);
       mk.mark(st);
       break;
+    }
     case Family::GemmTc: {
       CallMaps m;
       call_maps(k, d_in, n_in, d_out, ws, m);

@@ -395,6 +395,109 @@ __global__ void __launch_bounds__(256) k_simt_gemv(const GenericPlan p, const fl
   }
 }
 
+// gemv through TMA (plan.fast == 3: one row per thread per row group, i.e. vthreads == thread tile):
+// stage s holds, for row group e, the CTA's `slots` consecutive rows x 32 columns per 4 KB box
+// (128 B swizzle), 8 boxes per stage (256 columns); thread t reduces row (e * slots + t) from its
+// 128 B row of each box — the swizzle puts the 8 lanes of a shared-memory phase on distinct banks —
+// in ascending column order. Whole lines from HBM, one TMA op per 4 KB.
+constexpr int kGvBoxCols = 32, kGvBoxes = 8, kGvStages = 3;
+
+template <int TM>
+__global__ void __launch_bounds__(256) k_simt_gemv_tma(const __grid_constant__ CUtensorMap mapA, const GenericPlan p,
+                                                       const float* __restrict__ x, float* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // swizzle atoms
+  __shared__ uint64_t full[kGvStages], empty[kGvStages];
+  const int am = p.sp[0], an = p.red[0];
+  const int64_t M = p.ext[am], N = p.ext[an];
+  const int slots = p.slots;                        // rows per row group = threads that own rows
+  const uint32_t stage_bytes = static_cast<uint32_t>(slots) * 128 * kGvBoxes;
+  float* xs = reinterpret_cast<float*>(smem + kGvStages * stage_bytes);
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * p.B[0];
+  const int cols = kGvBoxCols * kGvBoxes;
+  const int nchunks = static_cast<int>((N + cols - 1) / cols);
+  const int nsteps = TM * nchunks;                  // (row group e, column chunk c), e-major
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGvStages; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], blockDim.x);
+    }
+    tc::fence_barrier_init();
+  }
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) xs[i] = x[i * p.coef[1][an]];
+  __syncthreads();
+  auto issue = [&](int s, int k) {  // thread 0: stage s <- step k
+    const int e = k / nchunks, c = k - e * nchunks;
+    tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
+    uint8_t* dst = smem + s * stage_bytes;
+    for (int b = 0; b < kGvBoxes; ++b)
+      tc::tma_load_2d(dst + b * slots * 128, &mapA, &full[s], c * cols + b * kGvBoxCols,
+                      static_cast<int>(m0 + static_cast<int64_t>(e) * slots));
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kGvStages && k < nsteps; ++k) issue(k, k);
+  const int t = threadIdx.x;
+  const bool active = t < slots;
+  float acc = 0.0f;
+  for (int k = 0; k < nsteps; ++k) {
+    const int s = k % kGvStages;
+    const int e = k / nchunks, c = k - e * nchunks;
+    tc::mbar_wait(&full[s], (k / kGvStages) & 1);
+    if (active) {
+      const uint8_t* src = smem + s * stage_bytes + t * 128;
+      const int64_t n0 = static_cast<int64_t>(c) * cols;
+      if (n0 + cols <= N) {
+#pragma unroll
+        for (int b = 0; b < kGvBoxes; ++b) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 v = *reinterpret_cast<const float4*>(src + b * slots * 128 + ((g ^ (t & 7)) << 4));
+            const float4 xx = *reinterpret_cast<const float4*>(xs + n0 + b * kGvBoxCols + 4 * g);
+            acc = fmaf(v.x, xx.x, acc);
+            acc = fmaf(v.y, xx.y, acc);
+            acc = fmaf(v.z, xx.z, acc);
+            acc = fmaf(v.w, xx.w, acc);
+          }
+        }
+      } else {
+        for (int q = 0; n0 + q < N; ++q) {
+          const int b = q / kGvBoxCols, w = q % kGvBoxCols;
+          const float v = *reinterpret_cast<const float*>(src + b * slots * 128 + (((w >> 2) ^ (t & 7)) << 4) + (w & 3) * 4);
+          acc = fmaf(v, xs[n0 + q], acc);
+        }
+      }
+      if (c == nchunks - 1) {  // row (e, t) complete
+        const int64_t m = m0 + static_cast<int64_t>(e) * slots + t;
+        if (m < M) y[m * p.coef[2][am]] = acc;
+        acc = 0.0f;
+      }
+    }
+    tc::mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && k + kGvStages < nsteps) {
+      tc::mbar_wait(&empty[s], (k / kGvStages) & 1);
+      issue(s, k + kGvStages);
+    }
+  }
+}
+
+void launch_simt_gemv_tma(const GenericPlan& p, const CUtensorMap& mapA, const void* in1, void* out, int batch,
+                          cudaStream_t st) {
+  dim3 g(static_cast<unsigned>(p.tiles[0]), static_cast<unsigned>(batch));
+  auto go = [&](auto kern) {
+    set_smem_attr(kern, p.smem_bytes, "simt gemv smem attribute");
+    kern<<<g, p.block, p.smem_bytes, st>>>(mapA, p, static_cast<const float*>(in1), static_cast<float*>(out));
+    check_cuda(cudaGetLastError(), "simt gemv launch");
+    count_launch();
+  };
+  switch (p.T[0]) {
+    case 1: go(k_simt_gemv_tma<1>); break;
+    case 2: go(k_simt_gemv_tma<2>); break;
+    case 4: go(k_simt_gemv_tma<4>); break;
+    case 8: go(k_simt_gemv_tma<8>); break;
+    default: throw Error(Code::Unsupported, "simt gemv thread tile");
+  }
+}
+
 template <typename In>
 void launch_simt_gemm(const GenericPlan& p, const void* in0, const void* in1, void* out, int batch, cudaStream_t st) {
   dim3 g(static_cast<unsigned>(p.tiles[0]) * static_cast<unsigned>(p.tiles[1]), static_cast<unsigned>(batch));
@@ -474,7 +577,11 @@ void dispatch(const GenericPlan& p, int width, const void* in0, const void* in1,
 int generic_max_width(bool f64) { return f64 ? 16 : 32; }
 
 void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, const void* in1, void* out,
-                    int batch, cudaStream_t st) {
+                    int batch, cudaStream_t st, const CUtensorMap* map) {
+  if (!f64 && !bf16 && p.fast == 3 && map) {
+    launch_simt_gemv_tma(p, *map, in1, out, batch, st);
+    return;
+  }
   if (!f64 && p.fast == 1) {
     if (bf16)
       launch_simt_gemm<__nv_bfloat16>(p, in0, in1, out, batch, st);

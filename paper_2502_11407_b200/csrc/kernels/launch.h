@@ -24,7 +24,7 @@ struct Marks {
 // ---- state-driven SIMT family (generic.cu) ----
 int generic_max_width(bool f64);
 void launch_generic(const GenericPlan& p, bool f64, bool bf16, const void* in0, const void* in1, void* out,
-                    int batch, cudaStream_t st);
+                    int batch, cudaStream_t st, const CUtensorMap* map = nullptr);
 
 // ---- TMA tensor maps (gemm_tc.cu) ----
 void encode_map(CUtensorMap* map, bool bf16, bool tf32, const void* ptr, int rank, const uint64_t* dims,
