@@ -243,6 +243,186 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// CTA pairs (cta_group::2): a cluster of two CTAs computes a 256 x BN tile; the leader issues
+// UMMA M = 256 (its 128 rows, then the peer's), each CTA stages its own 128 rows of A and HALF of
+// the tile's B columns (the UMMA splits B by columns across the pair), so per SM the B bytes
+// staged and read per k-block halve. Both producers' TMA loads complete on the leader's full
+// barrier; the leader's commits multicast to both CTAs' empty / accumulator-full barriers; both
+// CTAs' epilogue warps release an accumulator on the leader's barrier. The epilogue is k_gemm_tc's.
+template <typename T, typename TOut, int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_tc_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int tiles_m2, int tiles_n,
+                   int total, int a_batched) {
+  constexpr int BM = 128;                       // rows per CTA (UMMA M = 2 * BM)
+  constexpr int BK = 128 / sizeof(T);
+  constexpr uint32_t A_BYTES = BM * 128;
+  constexpr uint32_t B_BYTES = (BN / 2) * 128;  // this CTA's half of the B tile
+  constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  constexpr int B_CHUNKS = (BN / 2) * sizeof(T) / 128;
+  static_assert(B_CHUNKS >= 1, "pair B half must hold whole 128 B column chunks");
+  constexpr uint32_t ACC_COLS = BN;
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;
+  constexpr uint32_t IDESC = instr_desc(TcTraits<T>::kFormat, 2 * BM, BN, 0, 1);
+  constexpr int OUT_BLOCKS = BN * sizeof(TOut) / 128;
+  constexpr uint32_t STG_WARP = 32 * BN * sizeof(TOut);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* staging = smem + STAGES * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + 4 * STG_WARP);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nk = (K + BK - 1) / BK;
+  const int per_batch = tiles_m2 * tiles_n;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 8);  // the four epilogue warps of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    tma_prefetch(&mapC);
+  }
+  cluster_sync();  // both CTAs' barriers initialised before any cross-CTA completion
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
+        const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM, n0 = nt * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
+          uint8_t* a_s = smem + s * STAGE;
+          uint8_t* b_s = a_s + A_BYTES;
+          tma_load_3d_pair(a_s, &mapA, &full[s], kb * BK, m0, b * a_batched);
+#pragma unroll
+          for (int j = 0; j < B_CHUNKS; ++j)
+            tma_load_3d_pair(b_s + j * (BK * 128), &mapB, &full[s], n0 + j * (128 / (int)sizeof(T)), kb * BK, b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && elect_one()) {
+      int it = 0, local = 0;
+      for (int t = pair; t < total; t += npairs, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * STAGE);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = TcTraits<T>::kF16Kind
+                                    ? smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 1024, 2)
+                                    : smem_desc_sw128(b_addr + k * (4096 / sizeof(T)), BK * 128, 512, 1);
+            if constexpr (TcTraits<T>::kF16Kind)
+              mma_f16_pair(d, ad, bd, IDESC, (kb | k) != 0);
+            else
+              mma_tf32_pair(d, ad, bd, IDESC, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[s], 3);
+        }
+        mma_commit_pair(&acc_full[acc], 3);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int local = 0;
+    for (int t = pair; t < total; t += npairs, ++local) {
+      const int acc = local & 1;
+      const int b = t / per_batch, mt = (t % per_batch) / tiles_n, nt = t % tiles_n;
+      const int m0 = mt * 2 * BM + static_cast<int>(rank) * BM, n0 = nt * BN;
+      mbar_wait(&acc_full[acc], (local >> 1) & 1);
+      tc_fence_after();
+      uint8_t* stg = staging + q * STG_WARP;
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16) + c, r);
+        tmem_ld_wait();
+        tmem_ld_pin(r);
+        if constexpr (sizeof(TOut) == 4) {
+          uint8_t* blk = stg + (c / 32) * (32 * 128) + lane * 128;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(blk + ((k ^ (lane & 7)) << 4)) =
+                make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        } else {
+          uint8_t* blk = stg + (c / 64) * (32 * 128) + lane * 128;
+          const int k0 = (c % 64) / 8;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t p[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * k + 2 * v]), __uint_as_float(r[8 * k + 2 * v + 1]));
+              p[v] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            *reinterpret_cast<uint4*>(blk + (((k0 + k) ^ (lane & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+          }
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&acc_empty[acc]);
+        else mbar_arrive_remote(&acc_empty[acc], 0);
+        if (m0 + q * 32 < M) {
+#pragma unroll
+          for (int j = 0; j < OUT_BLOCKS; ++j)
+            if (n0 + j * (128 / (int)sizeof(TOut)) < N)
+              tma_store_3d(&mapC, stg + j * (32 * 128), n0 + j * (128 / (int)sizeof(TOut)), m0 + q * 32, b);
+        }
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the pair's MMAs, commits and remote arrivals are done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<TMEM_COLS>(tmem);
+  }
+}
+
 // fp32-grade GEMM on the tf32 tensor cores ("3xTF32"), C = A.B with fp32 storage:
 //   warp 0      TMA producer (plain FLOAT32 maps: the fp32 bits land untouched);
 //   warps 2..5  converters: every staged element x -> hi = tf32(x) in place, lo = tf32(x - hi)
@@ -492,6 +672,32 @@ void run_cs(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   count_launch();
 }
 
+template <typename T, typename TOut, int BN, int STAGES>
+void run_pair(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
+  constexpr uint32_t STAGE = 128 * 128 + (BN / 2) * 128;
+  const size_t smem = STAGES * STAGE + 4 * 32 * BN * sizeof(TOut) + 1024 + 256;
+  auto kern = k_gemm_tc_pair<T, TOut, BN, STAGES>;
+  set_smem_attr(kern, static_cast<int>(smem), "gemm_tc pair smem attribute");
+  const int tiles_m2 = (a.M + 255) / 256, tiles_n = (a.N + BN - 1) / BN;
+  const int total = tiles_m2 * tiles_n * a.batch;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * std::min(total, a.sms / 2));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  check_cuda(cudaLaunchKernelEx(&cfg, kern, m.A, m.B, m.C, a.M, a.N, a.K, tiles_m2, tiles_n, total,
+                                a.a_shared ? 0 : 1),
+             "gemm_tc pair launch");
+  count_launch();
+}
+
 // Cluster multicast of A pays when the k-loop is long (A re-read from L2 for every n-tile) and
 // the n-tiles split into whole clusters; CS = cluster size along N.
 template <typename T, typename TOut, int BN, int STAGES>
@@ -503,6 +709,16 @@ void run(const GemmTcArgs& a, const GemmTcMaps& m, cudaStream_t st) {
   if constexpr (2 * STAGE + 2 * STG + 2048 <= 227 * 1024) {
     if (nk <= 2 && a.cs == 1) {  // epilogue-bound: double-buffered staging, 2 pipeline stages
       run_cs<T, TOut, BN, 2, 1, 2>(a, m, st);
+      return;
+    }
+  }
+  if constexpr ((BN / 2) * sizeof(T) >= 128) {
+    if (a.pair) {
+      constexpr size_t PSTAGE = 128 * 128 + (BN / 2) * 128;
+      constexpr int FIT = static_cast<int>((227 * 1024 - 2048 - STG) / PSTAGE);
+      constexpr int PS = FIT >= 8 ? 8 : FIT >= 6 ? 6 : 4;
+      static_assert(FIT >= 4, "gemm_tc pair stages do not fit shared memory");
+      run_pair<T, TOut, BN, PS>(a, m, st);
       return;
     }
   }

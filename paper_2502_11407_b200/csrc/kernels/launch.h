@@ -43,6 +43,7 @@ struct GemmTcArgs {
   bool bf16 = false;
   bool a_shared = false;  // A is one matrix for every batch entry (1x1 conv: the filter bank)
   bool x3 = false;        // fp32-grade 3xTF32 (hi/lo operand split in the kernel), BN = 64
+  bool pair = false;      // CTA pairs (cta_group::2): 256 x BN tiles, half of B staged per CTA
 };
 struct GemmTcMaps {
   CUtensorMap A, B, C, Am;  // Am: A slices for cluster multicast (box rows 128 / cs)
