@@ -163,6 +163,21 @@ Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s) {
     c.exec_seconds = c.est_seconds;
     return c;
   }
+  if (op.kind == Kind::Conv2d && tensor_unit(unit)) {
+    const ConvFlatPlan p = conv_flat_plan_of(op, s);
+    if (p.shape_ok) {  // the conv_flat program this state instantiates (filter groups, CTA pairs)
+      const double t = conv_flat_seconds(op, d, p);
+      const int64_t pos_tiles = op.param("N") * ((op.param("OH") * op.param("W") + 123) / 124);
+      const double ctas = static_cast<double>(p.FG * std::min<int64_t>(pos_tiles, d.sms / p.FG));
+      c.waves = std::ceil(static_cast<double>(p.FG * pos_tiles) / ctas);
+      c.occupancy = ctas / d.sms;
+      c.compute_seconds = t;
+      c.est_seconds = std::max(t, hbm_floor + kLaunchSeconds);
+      c.bottleneck = t >= hbm_floor + kLaunchSeconds ? -1 : 0;
+      c.exec_seconds = c.est_seconds;
+      return c;
+    }
+  }
   const int L = std::max(1, s.L);
   double ctas = static_cast<double>(op.batch);
   int64_t threads = 1, acc = 1;
@@ -201,7 +216,7 @@ Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s) {
     c.est_seconds = hbm_floor;
     c.bottleneck = 0;
   }
-  // the family `auto` runs: tensor-core conv (fixed-shape plans, state-independent), the
+  // the family `auto` runs: tensor-core conv outside conv_flat's shapes (fixed-shape plans), the
   // HBM-streaming family (bandwidth-bound), or this SIMT estimate
   if (op.kind == Kind::Conv2d && tensor_unit(unit))
     c.exec_seconds = conv_tc_seconds(op, d);

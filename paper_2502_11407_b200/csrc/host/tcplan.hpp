@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "../kernels/flat_table.h"
 #include "hw.hpp"
 #include "op.hpp"
 #include "sched.hpp"
@@ -140,6 +141,80 @@ inline double conv_tc_seconds(const OpDesc& op, const DeviceLimits& d) {
   const double in_bytes = static_cast<double>(n * c * op.param("H") * op.param("W")) * 4;
   const double prepass = (r > 1 || s > 1) ? 2.0 * in_bytes / d.hbm_bytes_per_s + kLaunchSeconds : kLaunchSeconds;
   return t + prepass;
+}
+
+// ---- conv_flat (kernels/conv_flat.cu): the stride-1 conv over flattened NCHW planes ----------
+// A complete state instantiates it as follows:
+//   level-1 f tile      -> the filter group width FN (16 / 32 / 64 filters, at most F rounded to
+//                          16): F splits into FG = ceil(F / FN) groups; each group is a set of
+//                          CTAs with its own resident filter bank, UMMA N = taps x FN per offset
+//                          group, and re-reads the input (from L2) once per group;
+//   level-1 h x w tile  -> UMMA M: a tile of >= 256 output positions pairs two 128-position
+//                          tiles on a CTA pair (cta_group::2, each CTA holds half of the bank)
+//                          when the filters are one 64-wide group of a 3x3 window; smaller tiles
+//                          run one 128-position tile per CTA.
+struct ConvFlatPlan {
+  bool shape_ok = false;  // stride 1, C % 32 == 0, F <= 64, 16 B plane pitch, not 1x1
+  int FN = 64, FG = 1;
+  bool pair = false;
+};
+
+inline bool conv_flat_shape(const OpDesc& op) {
+  if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || op.batch != 1 || op.stride != 1) return false;
+  const int64_t C = op.param("C"), F = op.param("F"), R = op.param("R"), S = op.param("S");
+  const int64_t H = op.param("H"), W = op.param("W");
+  return C % 32 == 0 && F >= 1 && F <= 64 && (H * W) % 4 == 0 && R * S <= dev::kFlatMaxTaps && R <= H && S <= W &&
+         (R > 1 || S > 1);
+}
+
+inline ConvFlatPlan conv_flat_plan_of(const OpDesc& op, const Sched& s) {
+  ConvFlatPlan p;
+  p.shape_ok = conv_flat_shape(op);
+  if (!p.shape_ok) return p;
+  const int64_t F = op.param("F"), F16 = (F + 15) / 16 * 16;
+  const int64_t tf = s.L ? std::min(s.tile(op, 1, 1), F) : F;
+  const int64_t th = s.L ? std::min(s.tile(op, 2, 1), op.ax[2].extent) : op.ax[2].extent;
+  const int64_t tw = s.L ? std::min(s.tile(op, 3, 1), op.ax[3].extent) : op.ax[3].extent;
+  p.FN = static_cast<int>(std::min<int64_t>(F16, std::clamp<int64_t>((tf + 15) / 16 * 16, 16, 64)));
+  p.FG = static_cast<int>((F + p.FN - 1) / p.FN);
+  p.pair = p.FG == 1 && p.FN == 64 && op.param("R") == 3 && op.param("S") == 3 && op.param("W") >= 6 &&
+           th * tw >= 256;
+  // the resident bank (half of it per CTA of a pair) next to the input ring (4 stages single, 6
+  // on pairs) and the epilogue records must fit the 227 KB of shared memory (conv_flat_plan)
+  const int64_t bank = op.param("C") / 32 * op.param("R") * op.param("S") * p.FN * 128;
+  auto fits = [&](bool pair) { return bank / (pair ? 2 : 1) + (pair ? 6 : 4) * 16384 + 12288 + 2048 <= 227 * 1024; };
+  if (p.pair && !fits(true)) p.pair = false;
+  p.shape_ok = fits(p.pair) && dev::flat_table(static_cast<int>(op.param("R")), static_cast<int>(op.param("S")),
+                                               static_cast<int>(op.param("W")), p.FN, p.pair).ok;
+  return p;
+}
+
+// Analytical time (s) of a conv_flat program. Per 128-position tile an SM's shared-memory
+// datapath carries the A stages (TMA writes), the A operand reads of every UMMA k-step, the
+// filter bank reads (halved on a CTA pair) and the epilogue's shuffles / records / stores; the
+// tile costs the slower of that at 128 B / clk and the tensor work (measured 4.7 k
+// vs 4.3 k modelled single-CTA, 3.5 k vs 3.7 k on pairs). Persistent CTAs: FG groups of
+// min(tiles, SMs / FG) CTAs; the first UMMA starts ~5 k cycles after launch (bank image, TMEM,
+// ring fill) and the last tile's epilogue trails the loop.
+inline double conv_flat_seconds(const OpDesc& op, const DeviceLimits& d, const ConvFlatPlan& p) {
+  const int R = static_cast<int>(op.param("R")), S = static_cast<int>(op.param("S"));
+  const int W = static_cast<int>(op.param("W")), C = static_cast<int>(op.param("C"));
+  const int64_t N = op.param("N"), OH = op.param("OH");
+  const dev::FlatTable tb = dev::flat_table(R, S, W, p.FN, p.pair);
+  const int nck = C / 32, T = R * S;
+  int ops0 = 0, ops1 = 0;
+  for (int g = 0; g < tb.ngroups; ++g) ops0 += tb.grp_nop[0][g], ops1 += tb.grp_nop[1][g];
+  const double a_tma = static_cast<double>(tb.ngroups) * nck * 16384.0;
+  const double a_rd = static_cast<double>(ops0 + (nck - 1) * ops1) * 4 * 4096.0;
+  const double b_rd = static_cast<double>(nck) * T * p.FN * 128.0 / (p.pair ? 2 : 1);
+  const double epi = 128.0 * p.FN * 4 * 4;
+  const double smem_clk = (a_tma + a_rd + b_rd + epi) / kTcL2BytesPerClkPerSm;
+  const double tensor_clk = 2.0 * 128 * T * p.FN * C / (d.tf32_tc_flops / d.sms / d.sm_clock_hz);
+  const double t_tile = std::max(smem_clk, tensor_clk) / d.sm_clock_hz;
+  const int64_t pos_tiles = N * ((OH * W + 123) / 124);
+  const int64_t ctas_g = std::max<int64_t>(1, std::min<int64_t>(pos_tiles, d.sms / p.FG));
+  const double rounds = std::ceil(static_cast<double>(pos_tiles) / static_cast<double>(ctas_g));
+  return 5000.0 / d.sm_clock_hz + (rounds + 1) * t_tile + kLaunchSeconds;
 }
 
 }  // namespace gb

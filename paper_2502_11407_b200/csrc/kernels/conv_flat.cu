@@ -24,6 +24,10 @@
 // the workspace) while the conv grid starts and streams its first input stages; the conv CTAs
 // then copy W' into shared memory with one bulk copy per 32-channel chunk.
 //
+// Filter groups: the plan may split F into FG groups of FN filters (the constructed state's
+// level-1 f tile): CTA b works on group b % FG with that group's resident bank and walks the
+// position tiles b / FG, b / FG + grid / FG, ...; every group re-reads the input tiles (L2).
+//
 // Roles: warp 0 = TMA producer (one 16 KB stage per (tile, 32-channel chunk, offset group)),
 // warp 1 = MMA issuer (a precomputed op table: accumulator column, filter rows, UMMA N, first-touch
 // flag), warps 2.. = epilogue (EPW warps per TMEM lane quarter, splitting the 16-filter blocks).
@@ -168,21 +172,22 @@ __global__ void __launch_bounds__(128) k_flat_filters(const float* __restrict__ 
   if (threadIdx.x == 0) atomicMin(&g_flat_filt[0], static_cast<unsigned long long>(gtimer()));
 #endif
   const int c4n = a.C >> 2;
-  const int total = a.FN * c4n * a.T;
+  const int total = a.FG * a.FN * c4n * a.T;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < total) {
   const int t = e % a.T;
   const int u = e / a.T;
-  const int f = u / c4n, c4 = u - f * c4n;
+  const int f = u / c4n, c4 = u - f * c4n;  // f = group * FN + row in the group
+  const int fg = f / a.FN, fl = f - fg * a.FN;
   uint4 v = make_uint4(0u, 0u, 0u, 0u);
   if (f < a.F) {
     const float* src = K + (static_cast<int64_t>(f) * a.C + 4 * c4) * a.T + t;
     v = make_uint4(f32_to_tf32(__ldg(src)), f32_to_tf32(__ldg(src + a.T)), f32_to_tf32(__ldg(src + 2 * a.T)),
                    f32_to_tf32(__ldg(src + 3 * a.T)));
   }
-  const int row = a.tb.tap_slot[t] * a.FN + f;
-  const size_t off = static_cast<size_t>(c4 >> 3) * a.T * a.FN * 128 + static_cast<size_t>(row) * 128 +
-                     ((((c4 & 7) ^ (row & 7))) << 4);
+  const int row = a.tb.tap_slot[t] * a.FN + fl;
+  const size_t off = static_cast<size_t>(fg) * a.grp_bytes + static_cast<size_t>(c4 >> 3) * a.T * a.FN * 128 +
+                     static_cast<size_t>(row) * 128 + ((((c4 & 7) ^ (row & 7))) << 4);
   *reinterpret_cast<uint4*>(Wp + off) = v;
 #ifdef GENSOR_DEV_OVERRIDES
   if ((threadIdx.x & 31) == 0) atomicMax(&g_flat_filt[1], static_cast<unsigned long long>(gtimer()));
@@ -258,6 +263,8 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
   uint64_t* bank_bar = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bank_bar + kFlatMaxChunks);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // filter group of this CTA and its position-tile stream (the grid is a multiple of FG)
+  const int fg = blockIdx.x % a.FG, t_first = blockIdx.x / a.FG, t_step = gridDim.x / a.FG;
   if (threadIdx.x == 0) FL_MARK(0);
   if (threadIdx.x == 0) FL_GT(50);
 
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     if (elect_one()) {
       tma_prefetch(&mapX);
       int it = 0;
-      for (int t = blockIdx.x; t < a.total; t += gridDim.x) {
+      for (int t = t_first; t < a.total; t += t_step) {
         const int n = t / a.tiles_img;
         const int p0 = (t - n * a.tiles_img) * kFlatStep;
         for (int ck = 0; ck < nck; ++ck) {
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         uint64_t* bb = &bank_bar[ck < kFlatMaxChunks ? ck : kFlatMaxChunks - 1];
         if (ck < kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blk);
         else if (ck == kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blk * (nck - ck));
-        bulk_g2s(bank + ck * blk, Wp + static_cast<size_t>(ck) * blk, blk, bb);
+        bulk_g2s(bank + ck * blk, Wp + static_cast<size_t>(fg) * a.grp_bytes + static_cast<size_t>(ck) * blk, blk, bb);
       }
       FL_MARK(1);
       FlatIssueCtx c;
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
       const uint64_t bdesc0 = smem_desc_sw128(smem_u32(bank), 16, 1024);
       c.it = 0;
       c.local = 0;
-      for (int t = blockIdx.x; t < a.total; t += gridDim.x, ++c.local) {
+      for (int t = t_first; t < a.total; t += t_step, ++c.local) {
         const int acc = c.local & 1;
         mbar_wait(&acc_empty[acc], ((c.local >> 1) & 1) ^ 1);
         if (c.local < 6) FL_MARK(8 + c.local);
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     const int plane_out = a.OH * a.OW;
     const uint32_t bm = tb.bmask;
     int local = 0;
-    for (int t = blockIdx.x; t < nloop; t += gridDim.x, ++local) {
+    for (int t = t_first; t < nloop; t += t_step, ++local) {
       const int acc = local & 1;
       const int n = t / a.tiles_img;
       const int p0 = (t - n * a.tiles_img) * kFlatStep;
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
 #pragma unroll
       for (int x = 0; x < kFlatNfbh; ++x) {
         if (x < nmine) {
-          const int f0 = (h + x * EPW) * 16;
+          const int f0 = fg * FN + (h + x * EPW) * 16;
           float* op = O + (static_cast<int64_t>(n) * a.F + f0) * plane_out + static_cast<int64_t>(hrow) * a.OW + wcol;
           if (a.F - f0 >= 16) {
 #pragma unroll
@@ -888,7 +895,8 @@ size_t flat_smem(const ConvFlatArgs& a, int stages) {
 // Host plan: the tap / op table for this W (flat_table.h), tiling, shared-memory ring depth, and
 // whether a compile-time-specialised kernel issues the MMAs (3x3, FN = 64, W >= S + 3: the table
 // depends on W mod 4 only).
-bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a) {
+bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a, int fn_req,
+                    bool allow_pair) {
   if (stride != 1 || C % 32 != 0 || F < 1 || F > 64 || R < 1 || S < 1 || R > H || S > W) return false;
   if ((static_cast<int64_t>(H) * W) % 4 != 0) return false;  // plane pitch must be 16 B aligned for TMA
   const int T = R * S;
@@ -900,6 +908,12 @@ bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride,
   a.N = N, a.C = C, a.H = H, a.W = W, a.F = F, a.R = R, a.S = S;
   a.OH = H - R + 1, a.OW = W - S + 1;
   a.FN = (F + 15) / 16 * 16;
+  if (fn_req > 0) {  // filter groups of fn_req filters (the state's level-1 f tile)
+    if (fn_req % 16 || fn_req > 64) return false;
+    a.FN = std::min(a.FN, fn_req);
+  }
+  a.FG = (F + a.FN - 1) / a.FN;
+  if (a.FG > sms) return false;
   a.T = T;
   a.nck = C / 32;
   a.tb = flat_table(R, S, W, a.FN);
@@ -909,9 +923,10 @@ bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride,
   a.total = N * a.tiles_img;
   a.sms = sms;
   if (const char* e = dev_env("GENSOR_FLAT_EXP")) a.exp = std::atoi(e);
-  a.sync_off = static_cast<size_t>(a.nck) * T * a.FN * 128;   // the bank image, then the completion counter
+  a.grp_bytes = static_cast<size_t>(a.nck) * T * a.FN * 128;
+  a.sync_off = a.FG * a.grp_bytes;  // the bank images of the FG groups, then the completion counter
   a.ws_bytes = a.sync_off + 256;
-  a.filt_blocks = (a.FN * (C / 4) * T + 127) / 128;
+  a.filt_blocks = (a.FG * a.FN * (C / 4) * T + 127) / 128;
   a.stages = 0;
   for (int s = 6; s >= 4; --s)
     if (flat_smem(a, s) <= 227 * 1024) {
@@ -921,7 +936,8 @@ bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride,
   if (a.stages < 4) return false;
   // specialised issue when the op table equals the class representative's (W mod 4)
   a.spec = -1;
-  if (R == 3 && S == 3 && a.FN == 64 && W >= S + 3 && a.stages == 4 && !(a.exp & 2048)) {
+  if (R == 3 && S == 3 && ((a.FN == 64 && a.stages == 4) || (a.FN == 32 && a.stages == 6)) && W >= S + 3 &&
+      !(a.exp & 2048)) {
     const FlatTable rep = flat_table(R, S, flat_rep_w(S, W & 3), a.FN);
     bool same = rep.ok && rep.ngroups == a.tb.ngroups && rep.bmask == a.tb.bmask;
     for (int g = 0; same && g < rep.ngroups; ++g)
@@ -936,7 +952,7 @@ bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride,
   }
   // CTA pairs (cta_group::2) on the specialised path: the pair table must equal its class
   // representative's as well (the kernel reads the runs, half-bank offsets and prezero blocks)
-  if (a.spec >= 0 && a.total >= 2 && !(a.exp & 8192)) {
+  if (allow_pair && a.spec >= 0 && a.FN == 64 && a.FG == 1 && a.total >= 2 && !(a.exp & 8192)) {
     const FlatTable tp = flat_table(R, S, W, a.FN, true);
     const FlatTable rp = flat_table(R, S, flat_rep_w(S, W & 3), a.FN, true);
     bool same = tp.ok && rp.ok && tp.ngroups == rp.ngroups && tp.bmask == rp.bmask && tp.prezero == rp.prezero &&
@@ -997,7 +1013,7 @@ void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void
     k_flat_filters<<<a.filt_blocks, 128, 0, st>>>(static_cast<const float*>(K), static_cast<uint8_t*>(ws), a, sync);
   check_cuda(cudaGetLastError(), "conv_flat filter launch");
   count_launch();
-  const int grid = a.pair ? 2 * std::min((a.total + 1) / 2, a.sms / 2) : std::min(a.total, a.sms);
+  const int grid = a.pair ? 2 * std::min((a.total + 1) / 2, a.sms / 2) : a.FG * std::min(a.total, a.sms / a.FG);
   auto launch = [&](auto kern) {
     set_smem_attr(kern, static_cast<int>(smem), "conv_flat smem attribute");
     cudaLaunchConfig_t cfg = {};
@@ -1034,11 +1050,15 @@ void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void
       default: throw Error(Code::Unsupported, "conv_flat pair: class");
     }
   } else {
-    switch (a.spec) {
+    switch (a.spec < 0 ? -1 : a.spec + (a.FN == 32 ? 4 : 0)) {
       case 0: launch(k_conv_flat<4, FlatSpec<3, 3, 0, 64>>); break;
       case 1: launch(k_conv_flat<4, FlatSpec<3, 3, 1, 64>>); break;
       case 2: launch(k_conv_flat<4, FlatSpec<3, 3, 2, 64>>); break;
       case 3: launch(k_conv_flat<4, FlatSpec<3, 3, 3, 64>>); break;
+      case 4: launch(k_conv_flat<6, FlatSpec<3, 3, 0, 32>>); break;
+      case 5: launch(k_conv_flat<6, FlatSpec<3, 3, 1, 32>>); break;
+      case 6: launch(k_conv_flat<6, FlatSpec<3, 3, 2, 32>>); break;
+      case 7: launch(k_conv_flat<6, FlatSpec<3, 3, 3, 32>>); break;
       default:
         switch (a.stages) {
           case 4: launch(k_conv_flat<4, void>); break;

@@ -308,15 +308,23 @@ bool conv1x1_gemm_ok(const OpDesc& op, bool bf16) {
 }
 
 // conv_flat (tf32, stride 1, C % 32 == 0, F <= 64, H*W % 4 == 0): flattened NCHW planes read in
-// place by TMA, one launch (no NHWC copy, no filter pre-pass)
-bool conv_flat_ok(const OpDesc& op, bool bf16, int sms, ConvFlatArgs* out) {
+// place by TMA (no NHWC copy); the bank conversion is a PDL-chained launch. With a state, its
+// level-1 tiles choose the program (tcplan.hpp conv_flat_plan_of: filter groups, CTA pairs).
+bool conv_flat_ok(const OpDesc& op, bool bf16, int sms, ConvFlatArgs* out, const Sched* s) {
   if (op.kind != Kind::Conv2d || op.dtype_bytes != 4 || bf16 || op.batch != 1) return false;
   if (dev_env("GENSOR_CONV_FLAT") && dev_env("GENSOR_CONV_FLAT")[0] == '0') return false;  // A/B
+  int fn = 0;
+  bool pair = true;
+  if (s) {
+    const ConvFlatPlan p = conv_flat_plan_of(op, *s);
+    fn = p.FN;
+    pair = p.pair;
+  }
   ConvFlatArgs a;
   if (!conv_flat_plan(static_cast<int>(op.param("N")), static_cast<int>(op.param("C")),
                       static_cast<int>(op.param("H")), static_cast<int>(op.param("W")),
                       static_cast<int>(op.param("F")), static_cast<int>(op.param("R")),
-                      static_cast<int>(op.param("S")), static_cast<int>(op.stride), sms, a))
+                      static_cast<int>(op.param("S")), static_cast<int>(op.stride), sms, a, fn, pair))
     return false;
   if (a.R < 2 && a.S < 2) return false;  // 1x1: gemm_tc / conv_gemm
   if (out) *out = a;
@@ -478,14 +486,14 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
              << ",\"grid\":" << std::min<int64_t>(g.pair ? 2 * (tiles(g.BN) / 2) : tiles(g.BN), sms)
              << ",\"block\":192,\"persistent\":true,\"cluster_n\":" << g.cs
              << ",\"cta_pair\":" << (g.pair ? "true" : "false") << "}";
-        } else if (op.kind == Kind::Conv2d && conv_flat_ok(op, bf16, sms, &k->flat)) {
+        } else if (op.kind == Kind::Conv2d && conv_flat_ok(op, bf16, sms, &k->flat, &s)) {
           k->family = Family::ConvFlat;
           k->launch_names = {"conv_flat"};
           const ConvFlatArgs& c = k->flat;
           k->launches = 2;  // bank conversion + conv (programmatic dependent launch), timed as one span
           k->ws_bytes = c.ws_bytes;
           pi << "{\"family\":\"conv_flat\",\"M_tile\":\"128 wide positions of one image (124 outputs)\",\"FN\":"
-             << c.FN << ",\"tap_groups\":[";
+             << c.FN << ",\"filter_groups\":" << c.FG << ",\"tap_groups\":[";
           for (int g = 0; g < c.tb.ngroups; ++g) {
             pi << (g ? "," : "") << "{\"a\":" << (c.tb.group_o[g] & ~3) << ",\"umma\":[";
             for (int o = c.tb.grp_op0[1][g]; o < c.tb.grp_op0[1][g] + c.tb.grp_nop[1][g]; ++o)
@@ -493,7 +501,9 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
                  << "}";
             pi << "]}";
           }
-          pi << "],\"tiles\":" << c.total << ",\"grid\":" << std::min(c.total, sms) << ",\"stages\":" << c.stages
+          pi << "],\"tiles\":" << c.FG * c.total << ",\"grid\":"
+             << (c.pair ? 2 * std::min((c.total + 1) / 2, sms / 2) : c.FG * std::min(c.total, sms / c.FG))
+             << ",\"stages\":" << c.stages
              << ",\"mma_issue\":\"" << (c.spec >= 0 ? "specialised (3x3, W mod 4)" : "table-driven")
              << "\",\"cta_pair\":" << (c.pair ? "true" : "false") << ",\"prezero\":" << c.tb.prezero
              << ",\"grid_note\":\"" << (c.pair ? "clusters of 2 CTAs, UMMA M = 256 (cta_group::2), half the bank per CTA" : "one CTA per tile stream")

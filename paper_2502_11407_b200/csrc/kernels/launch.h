@@ -94,7 +94,8 @@ void launch_conv_tc(const ConvTcArgs& a, const ConvTcMaps& m, const void* I, con
 // ---- flattened-plane stride-1 tf32 conv2d reading NCHW in place, one launch (conv_flat.cu) ----
 struct ConvFlatArgs {
   int N = 0, C = 0, H = 0, W = 0, F = 0, R = 0, S = 0, OH = 0, OW = 0;
-  int FN = 0;    // filter rows per tap slot (F rounded up to 16)
+  int FN = 0;    // filter rows per tap slot: one filter group (F rounded up to 16, or the state's f tile)
+  int FG = 1;    // filter groups (ceil(F / FN)): CTA b works on group b % FG with that group's bank
   int T = 0;     // taps R*S
   int nck = 0;   // 32-channel chunks
   int PW = 0;    // wide positions per image (OH * W)
@@ -104,10 +105,13 @@ struct ConvFlatArgs {
   int exp = 0;   // DEV build only (GENSOR_FLAT_EXP): 2048 table-driven issue, 8192 single CTAs, 65536 timeline marker
   size_t ws_bytes = 0;  // bank image W' (workspace), rewritten by every execute, + completion counter
   size_t sync_off = 0;  // counter of filter CTAs done (handle-owned workspaces)
+  size_t grp_bytes = 0; // one filter group's bank image
   int filt_blocks = 0;  // CTAs of the bank-conversion launch
   FlatTable tb;         // taps, groups and the MMA op table for this W (flat_table.h)
 };
-bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a);
+// fn_req: filter group width (0 = all filters in one group), allow_pair: CTA pairs when legal
+bool conv_flat_plan(int N, int C, int H, int W, int F, int R, int S, int stride, int sms, ConvFlatArgs& a,
+                    int fn_req = 0, bool allow_pair = true);
 void conv_flat_map(const ConvFlatArgs& a, const void* I, CUtensorMap& mapX);
 void launch_conv_flat(const ConvFlatArgs& a, const CUtensorMap& mapX, const void* K, void* O, void* ws,
                       bool own_ws, cudaStream_t st, Marks& mk);

@@ -184,6 +184,74 @@ def test_baseline_configs_full_size(name, variant, tol):
     check(doc, variant, tol)
 
 
+# conv_flat programs chosen by the constructed state (tcplan.hpp conv_flat_plan_of): the level-1
+# f tile sets the filter group width FN (F splits into FG groups of CTAs, each with its own bank),
+# a >= 256-position level-1 h x w tile with one 64-wide group of a 3x3 window takes CTA pairs.
+FLAT_GROUP_CONVS = [
+    {"kind": "conv2d", "I": [2, 32, 12, 13], "K": [64, 32, 3, 3], "S": 1},   # W = 1 (mod 4)
+    {"kind": "conv2d", "I": [2, 64, 12, 15], "K": [64, 64, 3, 3], "S": 1},   # W = 3 (mod 4)
+    {"kind": "conv2d", "I": [3, 64, 16, 16], "K": [64, 64, 3, 3], "S": 1},   # W = 0 (mod 4)
+    {"kind": "conv2d", "I": [2, 32, 30, 30], "K": [64, 32, 3, 3], "S": 1},   # W = 2 (mod 4), 7 tiles / image
+    {"kind": "conv2d", "I": [2, 32, 12, 14], "K": [48, 32, 3, 3], "S": 1},   # last group partly past F
+    {"kind": "conv2d", "I": [1, 32, 9, 12], "K": [20, 32, 2, 2], "S": 1},    # FN 16, 4 taps
+    {"kind": "conv2d", "I": [1, 32, 20, 24], "K": [32, 32, 5, 5], "S": 1},   # 25 taps, table-driven issue
+    {"kind": "conv2d", "I": [2, 128, 10, 12], "K": [64, 128, 3, 3], "S": 1},  # whole-F bank too big: groups only
+]
+
+
+def _pow2(x):
+    p = 1
+    while p < x:
+        p *= 2
+    return p
+
+
+@pytest.mark.parametrize("split", [1, 2, 4])
+@pytest.mark.parametrize("doc", FLAT_GROUP_CONVS, ids=lambda d: json.dumps(d["I"] + d["K"]))
+def test_conv_flat_from_state(doc, split):
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    F, C, R, S = doc["K"][0], doc["I"][1], doc["K"][2], doc["K"][3]
+    tf = _pow2(F) // split
+    f16 = (F + 15) // 16 * 16
+    fn = min(f16, min(64, max(16, (tf + 15) // 16 * 16)))
+    fg = (F + fn - 1) // fn
+    bank = C // 32 * R * S * fn * 128
+    if bank + 4 * 16384 + 12288 + 2048 > 227 * 1024:
+        pytest.skip("the group's bank does not fit next to the ring")
+    trace = ([[0, 1, split]] if split > 1 else []) + [[3, -1, 0], [3, -1, 0]]
+    sched = g.from_trace(op, hw(), trace, mode="b200")
+    rng = np.random.default_rng(split)
+    for integer in (True, False):
+        xs = inputs(op, rng, integer=integer)
+        ref = O.reference_compute(doc, xs, threads=8)
+        got, info = run(op, sched, "tc_tf32", xs, ref.size)
+        plan = info["plan"]
+        assert plan["family"] == "conv_flat" and plan["FN"] == fn and plan["filter_groups"] == fg, plan
+        if fg > 1:
+            assert not plan["cta_pair"], plan
+        if integer:
+            assert np.array_equal(got, ref.astype(np.float32).astype(np.float64)), (plan, np.nanmax(np.abs(got - ref)))
+        else:
+            assert not np.isnan(got).any()
+            assert np.nanmax(np.abs(got - ref)) / np.abs(ref).max() <= TF32_TOL, plan
+
+
+def test_conv_flat_groups_distinct_programs():
+    """The headline conv's program follows the state: a state whose level-1 f tile is half of F
+    runs two filter groups, the construction's pick runs one group on CTA pairs; same results."""
+    doc = CONFIG_OPS["C"]
+    op = g.TensorOpSpec.parse_text(json.dumps(doc))
+    best = g.optimize(op, hw(), g.EngineConfig(seed=0, mode="b200", top_k=1))
+    split = g.from_trace(op, hw(), [[0, 1, 2], [3, -1, 0], [3, -1, 0]], mode="b200")
+    rng = np.random.default_rng(1)
+    xs = inputs(op, rng, integer=True)
+    a, ia = run(op, best, "tc_tf32", xs, int(np.prod(op.tensors[-1]["true_dims"])))
+    b, ib = run(op, split, "tc_tf32", xs, a.size)
+    assert ia["plan"]["filter_groups"] == 1 and ia["plan"]["cta_pair"], ia["plan"]
+    assert ib["plan"]["filter_groups"] == 2 and ib["plan"]["FN"] == 32, ib["plan"]
+    assert np.array_equal(a, b)
+
+
 def test_auto_picks_tensor_cores():
     for name in ("G", "C"):
         op = g.TensorOpSpec.parse_text(json.dumps(CONFIG_OPS[name]))
