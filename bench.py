@@ -302,11 +302,11 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
 
 def flush_l2(torch, flush):
     """Between timed steps: flush L2 (a 256 MiB write, outside the events), then keep the device
-    busy ~40 us (torch.cuda._sleep) so the host-side enqueue of the next execute overlaps device
+    busy ~100 us (torch.cuda._sleep) so the host-side enqueue of the next execute overlaps device
     work — the events then bracket device time only, not the Python call's latency (the e2e
     number is the one that includes the host path)."""
     flush.zero_()
-    torch.cuda._sleep(80_000)
+    torch.cuda._sleep(200_000)
 
 
 def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=(None, None)):
@@ -920,6 +920,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": e2e_ms,
                 "path": "gensor_execute_host (pinned host buffers)", "pipeline": res.get("host_pipe")},
         "gpu_launches": res["launches"],
+        "step_ms_distribution": {"median": statistics.median(res["step_ms"]), "min": min(res["step_ms"]),
+                                 "max": max(res["step_ms"])},
         "launch_breakdown_ms": {n: statistics.mean(v) for n, v in res["launch_ms"].items()},
         "construction_s": res["construct_s"],
         "schedule_index": res["index"], "rerank": res["rerank"],
