@@ -661,14 +661,15 @@ def run_suite_sharded(args, g, torch, hw, peaks, tf32, flush, device, ws, rank, 
 
     names = ["conv2d"] + SUITE_DEFAULT
     docs = [WORKLOADS[n]["op"] for n in names]
-    parts = shard.suite_partition(docs, hw, ws)
+    parts = shard.suite_partition(docs, hw, ws, [WORKLOADS[n].get("variant", "auto") for n in names])
     mine = parts[rank]
     results, total_ms = {}, 0.0
     barrier()
     with ClockSampler(local) as clk:
         for i in mine:
             spec = WORKLOADS[names[i]]
-            r = run_op(g, torch, spec, hw, args.steps, args.warmup, device, "auto", flush, e2e=False)
+            r = run_op(g, torch, spec, hw, args.steps, args.warmup, device, spec.get("variant", "auto"), flush,
+                       e2e=False)
             ms = statistics.mean(r["step_ms"])
             total_ms += ms
             results[names[i]] = {"ms": ms, "flops": r["flops"], "bytes": r["bytes"], "rank": rank,
@@ -749,13 +750,13 @@ def run_graph_vs_tree(args, g, torch, hw, flush, device):
         out[name] = {"unit": unit,
                      "graph": {"ms": t_graph, "value": unit_work / (t_graph / 1e3) / scale,
                                "schedule": graph[0]["state"]["repr"], "plan": p_graph,
-                               "est_ms": graph[0]["cost"]["est_seconds"] * 1e3},
+                               "est_ms": graph[0]["cost"].get("exec_seconds", graph[0]["cost"]["est_seconds"]) * 1e3},
                      "graph_reranked": {"ms": t_rerank, "value": unit_work / (t_rerank / 1e3) / scale,
                                         "schedule": graph[rr["best"]]["state"]["repr"], "index": rr["best"],
                                         "plan": p_rerank},
                      "tree": {"ms": t_tree, "value": unit_work / (t_tree / 1e3) / scale,
                               "schedule": tree[0]["state"]["repr"], "plan": p_tree,
-                              "est_ms": tree[0]["cost"]["est_seconds"] * 1e3},
+                              "est_ms": tree[0]["cost"].get("exec_seconds", tree[0]["cost"]["est_seconds"]) * 1e3},
                      "topk_rerank_ms": rr["ms"], "topk_distinct_plans": len(distinct),
                      "graph_over_tree": t_tree / t_graph, "reranked_over_tree": t_tree / t_rerank}
     geo = float(np.exp(np.mean([np.log(v["graph_over_tree"]) for v in out.values()])))

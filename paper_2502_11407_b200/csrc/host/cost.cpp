@@ -220,8 +220,13 @@ Cost estimate_b200(const OpDesc& op, const HwModel& hw, const Sched& s) {
   // HBM-streaming family (bandwidth-bound), or this SIMT estimate
   if (op.kind == Kind::Conv2d && tensor_unit(unit))
     c.exec_seconds = conv_tc_seconds(op, d);
-  else if (unit == ExecUnit::Hbm)
-    c.exec_seconds = hbm_floor + kLaunchSeconds;
+  else if (unit == ExecUnit::Hbm) {
+    // the HBM-streaming family (row / window ops): every byte once at the family's measured
+    // fraction of the copy bandwidth, whatever the work-unit size the state picks
+    // (est_seconds keeps the state's SIMT-style estimate: it ranks the states, which only pick
+    // the work-unit size here, and is the program `simt_f32` would run)
+    c.exec_seconds = hbm_floor / kStreamHbmEff + kLaunchSeconds;
+  }
   else
     c.exec_seconds = c.est_seconds + kLaunchSeconds;
   return c;

@@ -60,7 +60,10 @@ constexpr double kTcKBlockFloorClk = 256.0;      // measured per-k-block floor o
                                                  // cluster 1 and 4): barrier / TMA issue bound
 constexpr double kTcStoreBytesPerClkPerSm = 64.0;
 constexpr double kTcTmaLatencyClk = 1000.0;      // TMA box round trip + commit -> mbarrier
-constexpr double kLaunchSeconds = 3.0e-6;        // one kernel launch in a back-to-back stream
+constexpr double kLaunchSeconds = 5.0e-6;        // fixed cost of one execute: an empty 148-CTA kernel timed by
+                                                 // events after the bench's L2-flush write costs 5.1-5.9 us
+                                                 // (tools/launch_cost.cu; 3.8 us back to back)
+constexpr double kStreamHbmEff = 0.8;            // HBM-streaming family: measured 0.74-0.87 of the copy bandwidth
 constexpr int kTcRingBytes = 227 * 1024 - 2048;  // opt-in smem minus barriers / alignment
 
 struct GemmTcPlan {

@@ -53,5 +53,5 @@ for name, sched in states.items():
     print(json.dumps({"state": name, "schedule": sched[0]["state"]["repr"], "FN": p["FN"],
                       "filter_groups": p["filter_groups"], "cta_pair": p["cta_pair"], "grid": p["grid"],
                       "measured_us": round(t * 1e3, 2), "tflops": round(op.flops / (t * 1e-3) / 1e12, 1),
-                      "model_us": round(sched[0]["cost"]["est_seconds"] * 1e6, 2),
+                      "model_us": round(sched[0]["cost"]["exec_seconds"] * 1e6, 2),
                       "bit_identical_to_first": same}), flush=True)
