@@ -769,8 +769,11 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     const int nloop = nmine ? pairs_total : 0;
     const int plane_out = a.OH * a.OW;
     const uint32_t bm = tb.bmask;
+    // tiles of this CTA; the accumulator releases no MMA will wait for (the last two tiles') are
+    // skipped, so no remote arrive can be in flight when the pair exits
+    const int nlocal = nloop > pair ? (nloop - pair + npairs - 1) / npairs : 0;
     if (nmine) {
-      for (int acc = 0; acc < 2; ++acc) {
+      for (int acc = 0; acc < 2 && acc < nlocal; ++acc) {
         if (tb.prezero) prezero(acc);
         release(acc);
       }
@@ -808,8 +811,10 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
       for (int x = 0; x < kFlatNfbh; ++x)
 #pragma unroll
         for (int b = 0; b < 4; ++b) tmem_ld_pin(r[x][b]);
-      if (tb.prezero) prezero(acc);
-      release(acc);  // (no data is published: the TMEM reads are complete, a plain arrive suffices)
+      if (local + 2 < nlocal) {
+        if (tb.prezero) prezero(acc);
+        release(acc);  // (no data is published: the TMEM reads are complete, a plain arrive suffices)
+      }
       if (bm != 15u) {
 #pragma unroll
         for (int x = 0; x < kFlatNfbh; ++x)
@@ -875,7 +880,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // the pair's MMAs, TMEM reads and remote arrivals are done
+  cluster_sync_relaxed();  // the pair's MMAs, TMEM reads and every awaited remote arrival are done
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<512>(tmem);

@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(kNsThreads, 1)
       }
       if (warp == kMma + 1 && lane == 0 && local < 6) NS_MARK(32 + local);
     }
-    if (tma_store && lane == 0) bulk_wait<0>();  // output stores complete before the CTA retires
+    if (tma_store && lane == 0) bulk_wait_read<0>();  // the staging is read before the CTA retires
     if (warp == kMma + 1 && lane == 0) NS_MARK(40);
   }
   tc_fence_before();

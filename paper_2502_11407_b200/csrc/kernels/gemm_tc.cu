@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(192, 1)
         bulk_commit();
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // the staging is read; the global writes retire with the grid
   }
   tc_fence_before();
   __syncthreads();
@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else {
     const int q = warp & 3;
+    // the MMA of tile i + 2 waits for tile i's release: the last two tiles' releases are skipped,
+    // so no remote arrive can be in flight when the pair exits
+    const int nlocal = total > pair ? (total - pair + npairs - 1) / npairs : 0;
     int local = 0;
     for (int t = pair; t < total; t += npairs, ++local) {
       const int acc = local & 1;
@@ -401,8 +404,10 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (leader) mbar_arrive(&acc_empty[acc]);
-        else mbar_arrive_remote(&acc_empty[acc], 0);
+        if (local + 2 < nlocal) {
+          if (leader) mbar_arrive(&acc_empty[acc]);
+          else mbar_arrive_remote(&acc_empty[acc], 0);
+        }
         if (m0 + q * 32 < M) {
 #pragma unroll
           for (int j = 0; j < OUT_BLOCKS; ++j)
@@ -412,11 +417,11 @@ __global__ void __launch_bounds__(192, 1)
         bulk_commit();
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // the staging is read; the global writes retire with the grid
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // the pair's MMAs, commits and remote arrivals are done
+  cluster_sync_relaxed();  // the pair's MMAs, commits and every awaited remote arrival are done
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<TMEM_COLS>(tmem);
@@ -604,7 +609,7 @@ __global__ void __launch_bounds__(320, 1)
         bulk_commit();
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // the staging is read; the global writes retire with the grid
   }
   tc_fence_before();
   __syncthreads();
