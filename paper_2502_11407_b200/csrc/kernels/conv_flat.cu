@@ -138,7 +138,12 @@ __device__ __forceinline__ void flat_wait_bank_image(unsigned* sync, unsigned fi
   atomicMin(&g_flat_filt[4], static_cast<unsigned long long>(gtimer()));
 #endif
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the generic-proxy image -> this thread's bulk copies
-  if (atomicAdd(sync + 1, 1u) == gridDim.x - 1) {
+}
+
+// After this CTA's bank copies are issued (the returning atomic stays off the bank's critical
+// path): the last conv CTA through resets the counter for the next execute.
+__device__ __forceinline__ void flat_done_with_counter(unsigned* sync) {
+  if (sync && atomicAdd(sync + 1, 1u) == gridDim.x - 1) {
     atomicExch(sync, 0u);
     atomicExch(sync + 1, 0u);
   }
@@ -147,8 +152,8 @@ __device__ __forceinline__ void flat_wait_bank_image(unsigned* sync, unsigned fi
 __device__ __forceinline__ void flat_signal_bank_image(unsigned* sync) {
   __syncthreads();
   if (sync && threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(sync, 1u);
+    // release at gpu scope: cumulative over the CTA's image stores ordered before it by the barrier
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(sync) : "memory");
 #ifdef GENSOR_DEV_OVERRIDES
     atomicMax(&g_flat_filt[3], static_cast<unsigned long long>(gtimer()));
 #endif
@@ -321,6 +326,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         else if (ck == kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blk * (nck - ck));
         bulk_g2s(bank + ck * blk, Wp + static_cast<size_t>(fg) * a.grp_bytes + static_cast<size_t>(ck) * blk, blk, bb);
       }
+      flat_done_with_counter(sync);
       FL_MARK(1);
       FlatIssueCtx c;
       c.full = full;
@@ -729,6 +735,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         else if (ck == kFlatMaxChunks - 1) mbar_arrive_expect_tx(bb, blkh * (nck - ck));
         bulk_g2s(bank + ck * blkh, mine + static_cast<size_t>(ck) * blkh, blkh, bb);
       }
+      flat_done_with_counter(sync);
       if (!leader) {
         for (int ck = 0; ck < nck && ck < kFlatMaxChunks; ++ck) mbar_wait(&bank_bar[ck], 0);
         mbar_arrive_remote_release(peer_bar, 0);  // the leader's MMAs may read this bank half now
