@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     mbar_init(peer_bar, 1);
     fence_barrier_init();
   }
-  cluster_sync();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA completion
+  cluster_sync_relaxed();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA completion (init fence: release.cluster)
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
-  if constexpr (CS > 1) cluster_sync();  // peers' barriers are initialised before any multicast
+  if constexpr (CS > 1) cluster_sync_relaxed();  // peers' barriers are initialised before any multicast (init fence: release.cluster)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&mapB);
     tma_prefetch(&mapC);
   }
-  cluster_sync();  // both CTAs' barriers initialised before any cross-CTA completion
+  cluster_sync_relaxed();  // both CTAs' barriers initialised before any cross-CTA completion (init fence: release.cluster)
   if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
