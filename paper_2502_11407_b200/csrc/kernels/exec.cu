@@ -477,9 +477,11 @@ Kernel* prepare(const OpDesc& op, const Sched& s, int variant) {
           // tile splits into whole 128 B column chunks; a state asking for A multicast keeps it
           // (measured: GPT-2's GEMMs 4.23 -> 3.35 ms per step; at fewer pair tiles than SM pairs,
           // e.g. the 1024^3 GEMM, the single-CTA tiles fill more SMs and stay ahead)
+          const char* pe = dev_env("GENSOR_GEMM_PAIR");  // developer A/B: '0' never, '1' whenever legal
           g.pair = g.cs == 1 && g.M >= 256 && (g.BN / 2) * op.dtype_bytes >= 128 &&
-                   static_cast<int64_t>((g.M + 255) / 256) * ((g.N + g.BN - 1) / g.BN) * g.batch >= sms / 2 &&
-                   !(dev_env("GENSOR_GEMM_PAIR") && dev_env("GENSOR_GEMM_PAIR")[0] == '0');
+                   (static_cast<int64_t>((g.M + 255) / 256) * ((g.N + g.BN - 1) / g.BN) * g.batch >= sms / 2 ||
+                    (pe && pe[0] == '1')) &&
+                   !(pe && pe[0] == '0');
           pi << "{\"family\":\"gemm_tc\"" << (conv1x1 ? ",\"conv1x1\":\"O[n] = K . I[n], filter bank shared\"" : "")
              << ",\"BM\":" << (g.pair ? 256 : 128) << ",\"BN\":" << g.BN << ",\"BK_bytes\":128,\"stages\":"
              << gemm_tc_stages(g) << ",\"tiles\":" << (g.pair ? tiles(g.BN) / 2 : tiles(g.BN))
