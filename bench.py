@@ -302,11 +302,11 @@ def run_op(g, torch, spec, hw, steps, warmup, device, variant="auto", flush=None
 
 def flush_l2(torch, flush):
     """Between timed steps: flush L2 (a 256 MiB write, outside the events), then keep the device
-    busy ~100 us (torch.cuda._sleep) so the host-side enqueue of the next execute overlaps device
+    busy ~0.5 ms (torch.cuda._sleep) so the host-side enqueue of the next execute overlaps device
     work — the events then bracket device time only, not the Python call's latency (the e2e
     number is the one that includes the host path)."""
     flush.zero_()
-    torch.cuda._sleep(200_000)
+    torch.cuda._sleep(1_000_000)
 
 
 def roofline(res, spec, peaks, tf32_tflops, variant_name, traffic=(None, None)):
