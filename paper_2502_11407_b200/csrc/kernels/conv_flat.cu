@@ -56,6 +56,16 @@ using namespace tc;
 // 32+i epilogue done with tile i, 40 MMA loop end, 44/45 epilogue of tile 1: blocks read /
 // boundary values exchanged.
 __device__ long long g_flat_trace[160 * 64];
+// per epilogue warp, tile 1: [0] acc_full seen, [1] TMEM read, [2] at the quarter barrier, [3] past it, [4] done
+__device__ long long g_flat_warp[160 * 16 * 5];
+#define FL_WMARK(k)                                                                                   \
+  do {                                                                                                \
+    if (blockIdx.x < 160 && lane == 0 && local == 1 && warp >= 2)                                    \
+      g_flat_warp[(blockIdx.x * 16 + (warp - 2)) * 5 + (k)] = clock64() - g_flat_trace[blockIdx.x * 64]; \
+  } while (0)
+extern "C" int gensor_dev_flat_warp(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_flat_warp, sizeof(long long) * std::min(n, 160 * 16 * 5)) == cudaSuccess ? 0 : 19;
+}
 #define FL_MARK(slot) \
   do {                 \
     if (blockIdx.x < 160) g_flat_trace[blockIdx.x * 64 + (slot)] = clock64(); \
@@ -93,6 +103,9 @@ extern "C" int gensor_dev_flat_trace(long long* out, int n) {
   do {                 \
   } while (0)
 #define FL_CLOCK() 0ll
+#define FL_WMARK(k) \
+  do {              \
+  } while (0)
 #define FL_STORE(slot, v) \
   do {                     \
   } while (0)
@@ -800,6 +813,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
       const bool ok = own && j < vt && wcol < a.OW;
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       if (warp == 2 && lane == 0 && local < 6) FL_MARK(24 + local);
+      FL_WMARK(0);
       tc_fence_after();
       uint32_t r[kFlatNfbh][4][16];
 #pragma unroll
@@ -818,6 +832,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
       for (int x = 0; x < kFlatNfbh; ++x)
 #pragma unroll
         for (int b = 0; b < 4; ++b) tmem_ld_pin(r[x][b]);
+      FL_WMARK(1);
       if (local + 2 < nlocal) {
         if (tb.prezero) prezero(acc);
         release(acc);  // (no data is published: the TMEM reads are complete, a plain arrive suffices)
@@ -855,7 +870,9 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
           put16(mine + 48 + 16 * lane, r[x][3]);
         }
       }
+      FL_WMARK(2);
       named_bar(1 + h, 128);
+      FL_WMARK(3);
       if (lane < 3 && q < 3) {
 #pragma unroll
         for (int x = 0; x < kFlatNfbh; ++x) {
@@ -883,6 +900,7 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
         }
       }
       if (warp == 2 && lane == 0 && local < 6) FL_MARK(32 + local);
+      FL_WMARK(4);
     }
   }
   tc_fence_before();

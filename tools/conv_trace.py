@@ -108,3 +108,13 @@ if fam == "conv_flat":
     print("epilogue tile 1 (cycles from acc_full): blocks read", np.median(rel[:, 44] - e), "published", np.median(rel[:, 46] - e), "barrier", np.median(rel[:, 47] - e), "exchanged",
           np.median(rel[:, 45] - e), "done", np.median(rel[:, 33] - e))
 print("MMA issue->commit per tile: median", np.median(mma), " epilogue per tile: median", np.median(epi))
+if fam == "conv_flat" and hasattr(lib, "gensor_dev_flat_warp"):
+    fw = lib.gensor_dev_flat_warp
+    fw.argtypes = [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
+    wb = (ctypes.c_longlong * (160 * 16 * 5))()
+    assert fw(wb, 160 * 16 * 5) == 0
+    w = np.array(wb, dtype=np.int64).reshape(160, 16, 5)[:148]
+    print("per epilogue warp, tile 1 (cycles from CTA start; median over CTAs): got, TMEM read, at barrier, past barrier, done")
+    for i in range(16):
+        wi = i + 2
+        print(f"  warp {wi:2d} (q={wi & 3}, h={(wi - 2) >> 2}, SP{wi % 4}):", [int(np.median(w[:, i, k])) for k in range(5)])
