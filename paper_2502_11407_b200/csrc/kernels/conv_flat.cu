@@ -678,9 +678,12 @@ __global__ void __launch_bounds__(32 * (2 + 4 * kFlatEpw), 1)
     for (int i = 0; i < kFlatMaxChunks; ++i) mbar_init(&bank_bar[i], 1);
     mbar_init(peer_bar, 1);
     fence_barrier_init();
+    FL_MARK(5);
   }
-  cluster_sync_relaxed();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA completion (init fence: release.cluster)
+  cluster_sync_relaxed();
+  if (threadIdx.x == 0) FL_MARK(6);  // both CTAs' barriers initialised before any cross-CTA arrive / TMA completion (init fence: release.cluster)
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  if (threadIdx.x == 32) FL_MARK(7);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

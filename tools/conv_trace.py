@@ -118,3 +118,6 @@ if fam == "conv_flat" and hasattr(lib, "gensor_dev_flat_warp"):
     for i in range(16):
         wi = i + 2
         print(f"  warp {wi:2d} (q={wi & 3}, h={(wi - 2) >> 2}, SP{wi % 4}):", [int(np.median(w[:, i, k])) for k in range(5)])
+if fam == "conv_flat":
+    print("pair start (cycles from CTA start, median): barriers initialised", np.median(rel[:, 5]), "| cluster barrier passed",
+          np.median(rel[:, 6]), "| TMEM allocated (warp 1)", np.median(rel[:, 7]), "| block barrier passed", np.median(rel[:, 2]))
